@@ -1,0 +1,122 @@
+/* blasx_cuda.h — C ABI of the B200 tile engine (libblasx_cuda.so).
+ *
+ * The Python host runtime (paper_1510_05041_b200/, loaded with ctypes) keeps the
+ * reference's planner, scheduler and cache bookkeeping; everything that touches a GPU
+ * goes through these entry points.  Each one replaces a seam of the reference
+ * (paths relative to /root/reference/pkg/src/tileblas):
+ *
+ *   bx_init / bx_shutdown      memory.py:50-51 (one backing reservation per device),
+ *                              devices.py:102-118 (engines = streams), peer enablement
+ *   bx_host_register           (new) page-locking of caller operands, excluded from
+ *                              timing like the paper
+ *   bx_h2d_tile                tiling.py:192-204 tile_host_copy_in + scheduler.py:248-258
+ *   bx_d2h_tile                tiling.py:207-215 tile_host_copy_out + scheduler.py:488-505
+ *   bx_p2p_tile                scheduler.py:260-270 copy_from_peer / cache.py:312-322
+ *   bx_gemm_task               kernels.py:49-58 gemm_update (+ the k-loop of one task,
+ *                              routines.py:227-236), syrk/syr2k_update (kernels.py:67-102)
+ *                              via the triangle epilogue
+ *   bx_trsm_tile               kernels.py:105-161 trsm_solve
+ *   bx_materialize             kernels.py:164-211 (_masked_triangle / _symmetrized)
+ *   bx_event_*                 devices.py:150-166 sync_streams / drain_time; trace times
+ *   bx_last_error              errors.py exception messages
+ *
+ * Conventions: every call returns int status (BX_OK = 0; BX_EINVAL = 5 invalid argument,
+ * BX_ESINGULAR = 6, BX_ENOMEM = 7, BX_ECUDA = -1 any CUDA runtime error — message in
+ * bx_last_error).  No exception crosses the ABI.  Device memory is addressed as
+ * (device index, byte offset into that device's arena); the Python Arena is the
+ * authority for offsets.  Host pointers are borrowed and should be registered.  Every
+ * enqueue is asynchronous: it waits on `n_wait` event ids first and returns a completion
+ * event id through `ev_out` (pass NULL to skip).  Event ids are owned by the caller until
+ * bx_event_release.  Any host thread may call; ctypes drops the GIL for the call.
+ */
+#ifndef BLASX_CUDA_H
+#define BLASX_CUDA_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BX_OK 0
+#define BX_EINVAL 5
+#define BX_ESINGULAR 6
+#define BX_ENOMEM 7
+#define BX_ECUDA (-1)
+
+/* stream lanes per device: 0..n_compute-1 compute, then these */
+#define BX_LANE_H2D (-1)
+#define BX_LANE_D2H (-2)
+#define BX_LANE_P2P (-3)
+
+int bx_version(void);
+int bx_device_count(int* n);
+/* name (>=64 bytes), SM count, total and free HBM bytes */
+int bx_device_info(int dev, char* name, int name_len, int* sms, uint64_t* total_bytes,
+                   uint64_t* free_bytes);
+/* Create per-device engines: streams, event pool, singular flag, arena of arena_bytes[i]
+ * (0 = keep current), enable peer access between all pairs.  Idempotent; re-init with a
+ * larger arena grows the reservation. */
+int bx_init(int ndev, const int* device_ids, const uint64_t* arena_bytes, int n_compute);
+int bx_shutdown(void);
+int bx_arena_base(int dev, uint64_t* base);
+int bx_peer_enabled(int dev_a, int dev_b, int* enabled);
+
+int bx_host_register(void* ptr, uint64_t bytes);
+int bx_host_unregister(void* ptr);
+int bx_host_is_registered(const void* ptr, int* yes);
+
+/* strided host tile (column-major, host ld in elements) <-> contiguous device tile
+ * (column-major, device ld in elements) */
+int bx_h2d_tile(int dev, uint64_t dst_off, int dst_ld, const void* src, int64_t src_ld, int h,
+                int w, int elem_bytes, int n_wait, const int* wait, int* ev_out);
+int bx_d2h_tile(int dev, uint64_t src_off, int src_ld, void* dst, int64_t dst_ld, int h, int w,
+                int elem_bytes, int n_wait, const int* wait, int* ev_out);
+/* device->device copy over NVLink/NVSwitch (dst device's P2P lane) */
+int bx_p2p_tile(int dst_dev, uint64_t dst_off, int src_dev, uint64_t src_off, uint64_t bytes,
+                int n_wait, const int* wait, int* ev_out);
+
+/* one tile task: C = alpha * sum_s op(A_s) op(B_s) + beta * C on compute lane `stream`.
+ * ta/tb: operands stored transposed; tri: 0 full, 1 lower, 2 upper (diagonal tiles).
+ * Offsets in bytes into the arena; lds in elements; depth[s] = reduction extent of step s. */
+int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps,
+                 const uint64_t* a_off, const int* lda, const uint64_t* b_off, const int* ldb,
+                 const int* depth, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
+                 const int* wait, int* ev_out);
+/* in-place triangular solve of B (h x w) against the diagonal tile A */
+int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h,
+                 int w, double alpha, uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait,
+                 const int* wait, int* ev_out);
+/* dst (n x n) = op(tri(A)) [mode 0, unit diag substituted] or sym(A) [mode 1] */
+int bx_materialize(int dev, int stream, int mode_sym, int upper, int trans, int unit, int n,
+                   uint64_t a_off, int lda, uint64_t dst_off, int ldd, int n_wait, const int* wait,
+                   int* ev_out);
+/* singular flag set by bx_trsm_tile kernels of this device since the last reset */
+int bx_singular_flag(int dev, int reset, int* flag);
+
+/* events */
+int bx_event_record(int dev, int stream, int timing, int* ev_out);
+int bx_event_query(int ev);  /* 0 complete, 1 pending, <0 error */
+int bx_event_sync(int ev);
+int bx_event_wait_any(int n, const int* evs, int* index, int spin_us);
+int bx_event_elapsed(int ev0, int ev1, float* ms);
+int bx_event_release(int ev);
+int bx_stream_wait(int dev, int stream, int ev);
+int bx_device_sync(int dev);
+int bx_launch_count(uint64_t* n); /* kernels launched by this library since load */
+
+/* raw device buffers + device-resident GEMM (the HBM-resident bench leg) */
+int bx_dev_alloc(int dev, uint64_t bytes, uint64_t* ptr);
+int bx_dev_free(int dev, uint64_t ptr);
+int bx_dev_fill_uniform(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int stream);
+int bx_dev_copy_h2d(int dev, uint64_t dst, const void* src, uint64_t bytes);
+int bx_dev_copy_d2h(int dev, void* dst, uint64_t src, uint64_t bytes);
+int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, double alpha,
+                    uint64_t a, int lda, uint64_t b, int ldb, double beta, uint64_t c, int ldc);
+/* register-only DMMA loop: measured FP64 tensor peak for the roofline denominator */
+int bx_fp64_peak_probe(int dev, int iters, double* tflops);
+
+int bx_last_error(char* buf, int len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,754 @@
+// libblasx_cuda.so — the B200 tile engine behind include/blasx_cuda.h.
+// Per device: one arena reservation, n compute streams + H2D / D2H / P2P copy streams,
+// an event pool, a mapped-pinned singular flag.  See include/blasx_cuda.h for the seam
+// each entry point replaces in the reference.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/blasx_cuda.h"
+#include "bx_gemm_dmma.cuh"
+#include "bx_trsm.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err(BX_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" +     \
+                                   std::to_string((int)e_) + ")");                           \
+  } while (0)
+
+constexpr int kMaxCompute = 8;
+constexpr int kEvShift = 20;
+
+struct Device {
+  int cuda_id = -1;
+  int sms = 0;
+  int ncomp = 0;
+  cudaStream_t comp[kMaxCompute] = {};
+  cudaStream_t h2d = nullptr, d2h = nullptr, p2p = nullptr;
+  char* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  int* flag_host = nullptr;  // mapped pinned
+  int* flag_dev = nullptr;
+  std::vector<cudaEvent_t> events;  // id -> event
+  std::vector<int> timing;          // whether created with timing
+  std::vector<int> free_sync, free_timing;
+  unsigned attr_set = 0;  // cudaFuncSetAttribute done on this device (bit per kernel)
+  bool ready = false;
+};
+
+std::mutex g_mu;
+std::vector<Device> g_devs;  // index = logical device (order given to bx_init)
+std::map<const void*, uint64_t> g_registered;
+
+Device* dev_of(int d) {
+  if (d < 0 || d >= (int)g_devs.size() || !g_devs[d].ready) return nullptr;
+  return &g_devs[d];
+}
+
+cudaStream_t lane_stream(Device* D, int lane) {
+  if (lane == BX_LANE_H2D) return D->h2d;
+  if (lane == BX_LANE_D2H) return D->d2h;
+  if (lane == BX_LANE_P2P) return D->p2p;
+  if (lane >= 0 && lane < D->ncomp) return D->comp[lane];
+  return nullptr;
+}
+
+int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
+  Device* D = &g_devs[d];
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto& fl = timing ? D->free_timing : D->free_sync;
+  int idx;
+  if (!fl.empty()) {
+    idx = fl.back();
+    fl.pop_back();
+  } else {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+    if (err != cudaSuccess) return set_err(BX_ECUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(err));
+    idx = (int)D->events.size();
+    if (idx >= (1 << kEvShift)) return set_err(BX_ENOMEM, "event pool exhausted");
+    D->events.push_back(e);
+    D->timing.push_back(timing ? 1 : 0);
+  }
+  *ev = D->events[idx];
+  *id = (d << kEvShift) | idx;
+  return BX_OK;
+}
+
+bool ev_lookup(int id, cudaEvent_t* ev, int* d_out = nullptr) {
+  if (id < 0) return false;
+  int d = id >> kEvShift, idx = id & ((1 << kEvShift) - 1);
+  if (d >= (int)g_devs.size()) return false;
+  Device& D = g_devs[d];
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (idx >= (int)D.events.size()) return false;
+  *ev = D.events[idx];
+  if (d_out) *d_out = d;
+  return true;
+}
+
+int wait_all(cudaStream_t s, int n, const int* wait) {
+  for (int i = 0; i < n; ++i) {
+    cudaEvent_t e;
+    if (!ev_lookup(wait[i], &e)) return set_err(BX_EINVAL, "bad wait event id " + std::to_string(wait[i]));
+    CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
+  }
+  return BX_OK;
+}
+
+int finish(int d, cudaStream_t s, int* ev_out) {
+  if (!ev_out) return BX_OK;
+  cudaEvent_t e;
+  int id;
+  int rc = ev_get(d, false, &e, &id);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(e, s));
+  *ev_out = id;
+  return BX_OK;
+}
+
+// ---- kernel launchers (raw pointers) ---------------------------------------------------
+
+int current_dev_slot() {
+  int id = -1;
+  cudaGetDevice(&id);
+  for (size_t i = 0; i < g_devs.size(); ++i)
+    if (g_devs[i].ready && g_devs[i].cuda_id == id) return (int)i;
+  return -1;
+}
+
+// cudaFuncSetAttribute is per device: remember which kernels were configured where.
+bool need_attr(unsigned bit) {
+  int d = current_dev_slot();
+  if (d < 0) return true;
+  if (g_devs[d].attr_set & bit) return false;
+  g_devs[d].attr_set |= bit;
+  return true;
+}
+
+template <bool TA, bool TB>
+int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
+  if (need_attr(1u << ((TA ? 2 : 0) + (TB ? 1 : 0)))) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bx::G_SMEM_BYTES));
+  }
+  int tiles = ((t.h + bx::G_BM - 1) / bx::G_BM) * ((t.w + bx::G_BN - 1) / bx::G_BN);
+  bx::gemm_task_kernel<TA, TB><<<tiles, bx::G_THREADS, bx::G_SMEM_BYTES, s>>>(t);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+int launch_gemm(int ta, int tb, const bx::GemmTask& t, cudaStream_t s) {
+  if (t.h <= 0 || t.w <= 0) return BX_OK;
+  if (ta) return tb ? launch_gemm_t<true, true>(t, s) : launch_gemm_t<true, false>(t, s);
+  return tb ? launch_gemm_t<false, true>(t, s) : launch_gemm_t<false, false>(t, s);
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// General gemm over raw pointers, splitting step lists longer than G_MAX_STEPS into
+// several launches (later launches accumulate with beta = 1).
+int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, const double* const* a,
+             const int* lda, const double* const* b, const int* ldb, const int* depth, double alpha,
+             double beta, double* c, int ldc) {
+  if (h < 0 || w < 0 || nsteps < 0) return set_err(BX_EINVAL, "gemm: negative extent");
+  if (ldc < (h > 1 ? h : 1)) return set_err(BX_EINVAL, "gemm: ldc < h");
+  for (int i = 0; i < nsteps; ++i) {
+    if (depth[i] < 0) return set_err(BX_EINVAL, "gemm: negative depth");
+    int need_a = ta ? depth[i] : h, need_b = tb ? w : depth[i];
+    if (lda[i] < (need_a > 1 ? need_a : 1) || ldb[i] < (need_b > 1 ? need_b : 1))
+      return set_err(BX_EINVAL, "gemm: leading dimension too small");
+    if ((lda[i] & 1) || (ldb[i] & 1) || !aligned16(a[i]) || !aligned16(b[i]))
+      return set_err(BX_EINVAL, "gemm: operands must be 16-byte aligned with even leading dimensions");
+  }
+  if (nsteps == 0) {
+    // C = beta*C (beta==0 -> zero) — expressed as a zero-depth task
+    bx::GemmTask t{};
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.nsteps = 0; t.tri = tri; t.group_m = 8;
+    t.alpha = alpha; t.beta = beta;
+    return launch_gemm(ta, tb, t, s);
+  }
+  for (int s0 = 0; s0 < nsteps; s0 += bx::G_MAX_STEPS) {
+    bx::GemmTask t{};
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = 8;
+    t.alpha = alpha;
+    t.beta = (s0 == 0) ? beta : 1.0;
+    int n = nsteps - s0 < bx::G_MAX_STEPS ? nsteps - s0 : bx::G_MAX_STEPS;
+    t.nsteps = n;
+    for (int i = 0; i < n; ++i) {
+      t.steps[i].a = a[s0 + i]; t.steps[i].b = b[s0 + i];
+      t.steps[i].lda = lda[s0 + i]; t.steps[i].ldb = ldb[s0 + i]; t.steps[i].d = depth[s0 + i];
+    }
+    int rc = launch_gemm(ta, tb, t, s);
+    if (rc) return rc;
+  }
+  return BX_OK;
+}
+
+int scale_raw(cudaStream_t s, double* b, int ld, int h, int w, double alpha) {
+  dim3 blk(32, 8), grd((h + 31) / 32, (w + 7) / 8);
+  bx::scale_kernel<<<grd, blk, 0, s>>>(b, ld, h, w, alpha);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int h, int w, double alpha,
+              const double* a, int lda, double* b, int ldb, int* flag) {
+  bx::TrsmArgs t{};
+  t.a = a; t.b = b; t.lda = lda; t.ldb = ldb;
+  t.n = right ? w : h;
+  t.nrhs = right ? h : w;
+  t.swap = (trans != 0) != (right != 0);
+  t.rev = right ? !eff_upper : eff_upper;
+  t.right = right; t.unit = unit; t.alpha = alpha; t.flag = flag;
+  if (t.n == 0 || t.nrhs == 0) return BX_OK;
+  size_t smem = (size_t)t.n * bx::T_YP * sizeof(double);
+  if (need_attr(1u << 8)) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bx::T_NMAX * bx::T_YP * (int)sizeof(double)));
+  }
+  int grid = (t.nrhs + bx::T_NRHS - 1) / bx::T_NRHS;
+  bx::trsm_panel_kernel<<<grid, bx::T_THREADS, smem, s>>>(t);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+// Recursive blocked solve in physical coordinates (E = op(A) is eff_upper/lower); leaves of
+// order <= leaf_max run the panel kernel, the off-diagonal updates run the DMMA task GEMM.
+int trsm_rec(cudaStream_t s, int right, int eff_upper, int trans, int unit, int h, int w, double alpha,
+             const double* a, int lda, double* b, int ldb, int* flag, int leaf_max) {
+  int n = right ? w : h;
+  if (n <= leaf_max) return trsm_leaf(s, right, eff_upper, trans, unit, h, w, alpha, a, lda, b, ldb, flag);
+  if (alpha != 1.0) {
+    int rc = scale_raw(s, b, ldb, h, w, alpha);
+    if (rc) return rc;
+    alpha = 1.0;
+  }
+  int n1 = ((n / 2) + 31) / 32 * 32, n2 = n - n1;
+  // E block (r0, c0, rows, cols) -> A pointer + transpose flag
+  auto eblk = [&](int r0, int c0) -> const double* {
+    return trans ? a + (size_t)r0 * lda + c0 : a + (size_t)c0 * lda + r0;
+  };
+  const double* e11 = eblk(0, 0);
+  const double* e22 = eblk(n1, n1);
+  int rc;
+  if (!right) {
+    double* b1 = b;
+    double* b2 = b + n1;
+    if (!eff_upper) {
+      if ((rc = trsm_rec(s, 0, 0, trans, unit, n1, w, 1.0, e11, lda, b1, ldb, flag, leaf_max))) return rc;
+      const double* e21 = eblk(n1, 0);
+      int d = n1;
+      if ((rc = gemm_raw(s, trans, 0, 0, n2, w, 1, &e21, &lda, (const double* const*)&b1, &ldb, &d, -1.0, 1.0, b2, ldb))) return rc;
+      return trsm_rec(s, 0, 0, trans, unit, n2, w, 1.0, e22, lda, b2, ldb, flag, leaf_max);
+    }
+    if ((rc = trsm_rec(s, 0, 1, trans, unit, n2, w, 1.0, e22, lda, b2, ldb, flag, leaf_max))) return rc;
+    const double* e12 = eblk(0, n1);
+    int d = n2;
+    if ((rc = gemm_raw(s, trans, 0, 0, n1, w, 1, &e12, &lda, (const double* const*)&b2, &ldb, &d, -1.0, 1.0, b1, ldb))) return rc;
+    return trsm_rec(s, 0, 1, trans, unit, n1, w, 1.0, e11, lda, b1, ldb, flag, leaf_max);
+  }
+  double* b1 = b;
+  double* b2 = b + (size_t)n1 * ldb;
+  if (eff_upper) {
+    if ((rc = trsm_rec(s, 1, 1, trans, unit, h, n1, 1.0, e11, lda, b1, ldb, flag, leaf_max))) return rc;
+    const double* e12 = eblk(0, n1);
+    int d = n1;
+    if ((rc = gemm_raw(s, 0, trans, 0, h, n2, 1, (const double* const*)&b1, &ldb, &e12, &lda, &d, -1.0, 1.0, b2, ldb))) return rc;
+    return trsm_rec(s, 1, 1, trans, unit, h, n2, 1.0, e22, lda, b2, ldb, flag, leaf_max);
+  }
+  if ((rc = trsm_rec(s, 1, 0, trans, unit, h, n2, 1.0, e22, lda, b2, ldb, flag, leaf_max))) return rc;
+  const double* e21 = eblk(n1, 0);
+  int d = n2;
+  if ((rc = gemm_raw(s, 0, trans, 0, h, n1, 1, (const double* const*)&b2, &ldb, &e21, &lda, &d, -1.0, 1.0, b1, ldb))) return rc;
+  return trsm_rec(s, 1, 0, trans, unit, h, n1, 1.0, e11, lda, b1, ldb, flag, leaf_max);
+}
+
+__global__ void fill_uniform_kernel(double* p, uint64_t n, uint64_t seed) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    p[i] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+}
+
+__global__ void dmma_probe_kernel(double* out, int iters) {
+  double acc[8][2];
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) bx::dmma(acc[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bx_version(void) { return 1; }
+
+int bx_last_error(char* buf, int len) {
+  if (buf && len > 0) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return BX_OK;
+}
+
+int bx_launch_count(uint64_t* n) {
+  *n = g_launches.load();
+  return BX_OK;
+}
+
+int bx_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) { *n = 0; return set_err(BX_ECUDA, cudaGetErrorString(e)); }
+  *n = c;
+  return BX_OK;
+}
+
+int bx_device_info(int dev, char* name, int name_len, int* sms, uint64_t* total_bytes, uint64_t* free_bytes) {
+  cudaDeviceProp p;
+  CUDA_TRY(cudaGetDeviceProperties(&p, dev));
+  if (name && name_len > 0) { std::strncpy(name, p.name, name_len - 1); name[name_len - 1] = 0; }
+  if (sms) *sms = p.multiProcessorCount;
+  CUDA_TRY(cudaSetDevice(dev));
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+  if (total_bytes) *total_bytes = tot;
+  if (free_bytes) *free_bytes = fr;
+  return BX_OK;
+}
+
+int bx_init(int ndev, const int* device_ids, const uint64_t* arena_bytes, int n_compute) {
+  if (ndev <= 0 || n_compute <= 0 || n_compute > kMaxCompute) return set_err(BX_EINVAL, "bx_init: bad ndev/n_compute");
+  int count = 0;
+  CUDA_TRY(cudaGetDeviceCount(&count));
+  if ((int)g_devs.size() < ndev) g_devs.resize(ndev);
+  for (int d = 0; d < ndev; ++d) {
+    Device& D = g_devs[d];
+    int id = device_ids[d];
+    if (id < 0 || id >= count) return set_err(BX_EINVAL, "bx_init: no such CUDA device " + std::to_string(id));
+    if (D.ready && D.cuda_id != id) return set_err(BX_EINVAL, "bx_init: device slot remapped");
+    CUDA_TRY(cudaSetDevice(id));
+    if (!D.ready) {
+      D.cuda_id = id;
+      CUDA_TRY(cudaDeviceGetAttribute(&D.sms, cudaDevAttrMultiProcessorCount, id));
+      CUDA_TRY(cudaHostAlloc((void**)&D.flag_host, sizeof(int), cudaHostAllocMapped));
+      *D.flag_host = 0;
+      CUDA_TRY(cudaHostGetDevicePointer((void**)&D.flag_dev, D.flag_host, 0));
+      CUDA_TRY(cudaStreamCreateWithFlags(&D.h2d, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&D.d2h, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&D.p2p, cudaStreamNonBlocking));
+      D.ready = true;
+    }
+    for (int s = D.ncomp; s < n_compute; ++s) CUDA_TRY(cudaStreamCreateWithFlags(&D.comp[s], cudaStreamNonBlocking));
+    if (n_compute > D.ncomp) D.ncomp = n_compute;
+    uint64_t want = arena_bytes ? arena_bytes[d] : 0;
+    if (want > D.arena_bytes) {
+      if (D.arena) { CUDA_TRY(cudaDeviceSynchronize()); CUDA_TRY(cudaFree(D.arena)); D.arena = nullptr; D.arena_bytes = 0; }
+      cudaError_t e = cudaMalloc((void**)&D.arena, want);
+      if (e != cudaSuccess) {
+        D.arena = nullptr;
+        cudaGetLastError();
+        return set_err(BX_ENOMEM, "arena cudaMalloc of " + std::to_string(want) + " bytes failed: " + cudaGetErrorString(e));
+      }
+      D.arena_bytes = want;
+    }
+  }
+  for (int a = 0; a < ndev; ++a)
+    for (int b = 0; b < ndev; ++b) {
+      if (a == b) continue;
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, g_devs[a].cuda_id, g_devs[b].cuda_id));
+      if (!can) continue;
+      CUDA_TRY(cudaSetDevice(g_devs[a].cuda_id));
+      cudaError_t e = cudaDeviceEnablePeerAccess(g_devs[b].cuda_id, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return set_err(BX_ECUDA, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  return BX_OK;
+}
+
+int bx_shutdown(void) {
+  for (auto& D : g_devs) {
+    if (!D.ready) continue;
+    cudaSetDevice(D.cuda_id);
+    cudaDeviceSynchronize();
+    for (auto e : D.events) cudaEventDestroy(e);
+    for (int s = 0; s < D.ncomp; ++s) cudaStreamDestroy(D.comp[s]);
+    cudaStreamDestroy(D.h2d); cudaStreamDestroy(D.d2h); cudaStreamDestroy(D.p2p);
+    if (D.arena) cudaFree(D.arena);
+    if (D.flag_host) cudaFreeHost(D.flag_host);
+  }
+  g_devs.clear();
+  return BX_OK;
+}
+
+int bx_arena_base(int dev, uint64_t* base) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  *base = (uint64_t)D->arena;
+  return BX_OK;
+}
+
+int bx_peer_enabled(int a, int b, int* en) {
+  Device *A = dev_of(a), *B = dev_of(b);
+  if (!A || !B) return set_err(BX_EINVAL, "bad device");
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, A->cuda_id, B->cuda_id));
+  *en = can;
+  return BX_OK;
+}
+
+int bx_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return set_err(BX_EINVAL, "register: null");
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_registered.count(ptr)) return BX_OK;
+  }
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) { cudaGetLastError(); return BX_OK; }
+  if (e != cudaSuccess) { cudaGetLastError(); return set_err(BX_ECUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e)); }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_registered[ptr] = bytes;
+  return BX_OK;
+}
+
+int bx_host_unregister(void* ptr) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_registered.erase(ptr)) return BX_OK;
+  }
+  CUDA_TRY(cudaHostUnregister(ptr));
+  return BX_OK;
+}
+
+int bx_host_is_registered(const void* ptr, int* yes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  *yes = 0;
+  auto it = g_registered.upper_bound(ptr);
+  if (it != g_registered.begin()) {
+    --it;
+    if ((const char*)ptr < (const char*)it->first + it->second) *yes = 1;
+  }
+  return BX_OK;
+}
+
+int bx_h2d_tile(int dev, uint64_t dst_off, int dst_ld, const void* src, int64_t src_ld, int h, int w, int eb,
+                int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  if (h <= 0 || w <= 0 || dst_ld < h || src_ld < h) return set_err(BX_EINVAL, "h2d: bad extents");
+  if (dst_off + (uint64_t)dst_ld * w * eb > D->arena_bytes) return set_err(BX_EINVAL, "h2d: outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(D->h2d, n_wait, wait);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy2DAsync(D->arena + dst_off, (size_t)dst_ld * eb, src, (size_t)src_ld * eb, (size_t)h * eb, w,
+                             cudaMemcpyHostToDevice, D->h2d));
+  return finish(dev, D->h2d, ev_out);
+}
+
+int bx_d2h_tile(int dev, uint64_t src_off, int src_ld, void* dst, int64_t dst_ld, int h, int w, int eb, int n_wait,
+                const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  if (h <= 0 || w <= 0 || src_ld < h || dst_ld < h) return set_err(BX_EINVAL, "d2h: bad extents");
+  if (src_off + (uint64_t)src_ld * w * eb > D->arena_bytes) return set_err(BX_EINVAL, "d2h: outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(D->d2h, n_wait, wait);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dst_ld * eb, D->arena + src_off, (size_t)src_ld * eb, (size_t)h * eb, w,
+                             cudaMemcpyDeviceToHost, D->d2h));
+  return finish(dev, D->d2h, ev_out);
+}
+
+int bx_p2p_tile(int dst_dev, uint64_t dst_off, int src_dev, uint64_t src_off, uint64_t bytes, int n_wait,
+                const int* wait, int* ev_out) {
+  Device *D = dev_of(dst_dev), *S = dev_of(src_dev);
+  if (!D || !S) return set_err(BX_EINVAL, "bad device");
+  if (dst_off + bytes > D->arena_bytes || src_off + bytes > S->arena_bytes) return set_err(BX_EINVAL, "p2p: outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(D->p2p, n_wait, wait);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyPeerAsync(D->arena + dst_off, D->cuda_id, S->arena + src_off, S->cuda_id, bytes, D->p2p));
+  return finish(dst_dev, D->p2p, ev_out);
+}
+
+int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps, const uint64_t* a_off,
+                 const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, double alpha, double beta,
+                 uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  if (tri < 0 || tri > 2 || (tri && h != w)) return set_err(BX_EINVAL, "gemm: triangle mode needs a square tile");
+  if (nsteps > 4096) return set_err(BX_EINVAL, "gemm: too many steps");
+  std::vector<const double*> ap(nsteps > 0 ? nsteps : 1), bp(nsteps > 0 ? nsteps : 1);
+  for (int i = 0; i < nsteps; ++i) {
+    if (a_off[i] >= D->arena_bytes || b_off[i] >= D->arena_bytes) return set_err(BX_EINVAL, "gemm: operand outside arena");
+    ap[i] = (const double*)(D->arena + a_off[i]);
+    bp[i] = (const double*)(D->arena + b_off[i]);
+  }
+  if (c_off + (uint64_t)ldc * w * 8 > D->arena_bytes) return set_err(BX_EINVAL, "gemm: C outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  rc = gemm_raw(s, ta, tb, tri, h, w, nsteps, ap.data(), lda, bp.data(), ldb, depth, alpha, beta, (double*)(D->arena + c_off), ldc);
+  if (rc) return rc;
+  return finish(dev, s, ev_out);
+}
+
+int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h, int w, double alpha,
+                 uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  int n = side_right ? w : h;
+  if (lda < n || ldb < h || (lda & 1) || (ldb & 1)) return set_err(BX_EINVAL, "trsm: bad leading dimension");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  int eff_upper = (upper != 0) != (trans != 0);
+  rc = trsm_rec(s, side_right, eff_upper, trans, unit, h, w, alpha, (const double*)(D->arena + a_off), lda,
+                (double*)(D->arena + b_off), ldb, D->flag_dev, 1024);
+  if (rc) return rc;
+  return finish(dev, s, ev_out);
+}
+
+int bx_materialize(int dev, int stream, int mode_sym, int upper, int trans, int unit, int n, uint64_t a_off, int lda,
+                   uint64_t dst_off, int ldd, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  if (n <= 0 || lda < n || ldd < n) return set_err(BX_EINVAL, "materialize: bad extents");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  dim3 blk(32, 8), grd((n + 31) / 32, (n + 7) / 8);
+  bx::materialize_kernel<<<grd, blk, 0, s>>>((const double*)(D->arena + a_off), lda, (double*)(D->arena + dst_off), ldd,
+                                            n, mode_sym, upper, trans, unit);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return finish(dev, s, ev_out);
+}
+
+int bx_singular_flag(int dev, int reset, int* flag) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  *flag = *(volatile int*)D->flag_host;
+  if (reset) *(volatile int*)D->flag_host = 0;
+  return BX_OK;
+}
+
+int bx_event_record(int dev, int stream, int timing, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s) return set_err(BX_EINVAL, "bad stream");
+  cudaEvent_t e;
+  int id;
+  int rc = ev_get(dev, timing != 0, &e, &id);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaEventRecord(e, s));
+  *ev_out = id;
+  return BX_OK;
+}
+
+int bx_event_query(int ev) {
+  cudaEvent_t e;
+  if (!ev_lookup(ev, &e)) return set_err(BX_EINVAL, "bad event");
+  cudaError_t r = cudaEventQuery(e);
+  if (r == cudaSuccess) return 0;
+  if (r == cudaErrorNotReady) { cudaGetLastError(); return 1; }
+  return set_err(BX_ECUDA, std::string("event: ") + cudaGetErrorString(r));
+}
+
+int bx_event_sync(int ev) {
+  cudaEvent_t e;
+  if (!ev_lookup(ev, &e)) return set_err(BX_EINVAL, "bad event");
+  CUDA_TRY(cudaEventSynchronize(e));
+  return BX_OK;
+}
+
+int bx_event_wait_any(int n, const int* evs, int* index, int spin_us) {
+  if (n <= 0) return set_err(BX_EINVAL, "wait_any: empty");
+  std::vector<cudaEvent_t> es(n);
+  for (int i = 0; i < n; ++i)
+    if (!ev_lookup(evs[i], &es[i])) return set_err(BX_EINVAL, "bad event");
+  auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    for (int i = 0; i < n; ++i) {
+      cudaError_t r = cudaEventQuery(es[i]);
+      if (r == cudaSuccess) { *index = i; return BX_OK; }
+      if (r != cudaErrorNotReady) return set_err(BX_ECUDA, cudaGetErrorString(r));
+    }
+    cudaGetLastError();
+    if (spin_us >= 0) {
+      auto us = std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count();
+      if (us >= spin_us) { *index = -1; return BX_OK; }
+    }
+    std::this_thread::yield();
+  }
+}
+
+int bx_event_elapsed(int ev0, int ev1, float* ms) {
+  cudaEvent_t a, b;
+  if (!ev_lookup(ev0, &a) || !ev_lookup(ev1, &b)) return set_err(BX_EINVAL, "bad event");
+  CUDA_TRY(cudaEventElapsedTime(ms, a, b));
+  return BX_OK;
+}
+
+int bx_event_release(int ev) {
+  if (ev < 0) return BX_OK;
+  int d = ev >> kEvShift, idx = ev & ((1 << kEvShift) - 1);
+  if (d >= (int)g_devs.size()) return set_err(BX_EINVAL, "bad event");
+  Device& D = g_devs[d];
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (idx >= (int)D.events.size()) return set_err(BX_EINVAL, "bad event");
+  (D.timing[idx] ? D.free_timing : D.free_sync).push_back(idx);
+  return BX_OK;
+}
+
+int bx_stream_wait(int dev, int stream, int ev) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s) return set_err(BX_EINVAL, "bad stream");
+  cudaEvent_t e;
+  if (!ev_lookup(ev, &e)) return set_err(BX_EINVAL, "bad event");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
+  return BX_OK;
+}
+
+int bx_device_sync(int dev) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return BX_OK;
+}
+
+int bx_dev_alloc(int dev, uint64_t bytes, uint64_t* ptr) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) { cudaGetLastError(); return set_err(BX_ENOMEM, cudaGetErrorString(e)); }
+  *ptr = (uint64_t)p;
+  return BX_OK;
+}
+
+int bx_dev_free(int dev, uint64_t ptr) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaFree((void*)ptr));
+  return BX_OK;
+}
+
+int bx_dev_fill_uniform(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int stream) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s) return set_err(BX_EINVAL, "bad stream");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  fill_uniform_kernel<<<D->sms * 8, 256, 0, s>>>((double*)ptr, n, seed);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+int bx_dev_copy_h2d(int dev, uint64_t dst, const void* src, uint64_t bytes) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaMemcpy((void*)dst, src, bytes, cudaMemcpyHostToDevice));
+  return BX_OK;
+}
+
+int bx_dev_copy_d2h(int dev, void* dst, uint64_t src, uint64_t bytes) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaMemcpy(dst, (const void*)src, bytes, cudaMemcpyDeviceToHost));
+  return BX_OK;
+}
+
+int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, double alpha, uint64_t a, int lda,
+                    uint64_t b, int ldb, double beta, uint64_t c, int ldc) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  const double* ap = (const double*)a;
+  const double* bp = (const double*)b;
+  return gemm_raw(s, ta, tb, 0, m, n, 1, &ap, &lda, &bp, &ldb, &k, alpha, beta, (double*)c, ldc);
+}
+
+int bx_fp64_peak_probe(int dev, int iters, double* tflops) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  double* out;
+  CUDA_TRY(cudaMalloc(&out, 4096));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  cudaStream_t s = D->comp[0];
+  dmma_probe_kernel<<<D->sms * 2, 256, 0, s>>>(out, iters);
+  g_launches++;
+  CUDA_TRY(cudaEventRecord(e0, s));
+  dmma_probe_kernel<<<D->sms * 2, 256, 0, s>>>(out, iters);
+  g_launches++;
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  *tflops = (double)D->sms * 2 * 8 * (double)iters * 8 * 512.0 / ms / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return BX_OK;
+}
+
+}  // extern "C"
