@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: host-resident tiled DGEMM on B200 (BASELINE.json configs[1]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg1|dgemm32768|cfg3_syrk|cfg3_syr2k|cfg4_trsm|cfg4_trmm]
+
+Prints ONE JSON line (rank 0).  Legs:
+  value     device-resident DGEMM over the same workload (inputs already in HBM; the
+            dominant tile kernel, FP64 DMMA) — whole-job TFLOP/s over the N GPUs;
+  e2e       the public API call (``dgemm`` / ``run_call``) on host-resident numpy buffers,
+            H2D tile loads + D2H write-back inside the timed region — the headline;
+  roofline  dominant kernel: flops per launch / CUDA-event launch time vs the FP64 DMMA
+            peak measured live (MEASURED_PEAKS.json has no FP64 figure);
+  cpu_baseline  the oracle port of the reference tiled runtime (numpy/OpenBLAS, all host
+            cores) on a bounded sample of the same workload.
+Under torchrun (WORLD_SIZE>1) rank 0 drives all N GPUs from one process — BLASX is a
+single-address-space multi-GPU runtime (the L2 tile cache is peer HBM) — and the other
+ranks only join the barriers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(kind="gemm", m=2048, n=2048, k=2048, tile=512, alpha=1.0, beta=1.0,
+                 desc="DGEMM 2048x2048x2048 NN, tile 512, alpha=1 beta=1 (BASELINE configs[0])"),
+    "cfg2": dict(kind="gemm", m=16384, n=16384, k=16384, tile=1024, alpha=1.0, beta=1.0,
+                 desc="DGEMM 16384^3 NN host-resident, tile 1024, alpha=1 beta=1 (BASELINE configs[1])"),
+    "dgemm32768": dict(kind="gemm", m=32768, n=32768, k=32768, tile=1024, alpha=1.0, beta=1.0,
+                       desc="DGEMM 32768^3 NN host-resident, tile 1024 (north-star target)"),
+    "cfg3_syrk": dict(kind="syrk", m=16384, n=16384, k=8192, tile=1024, alpha=1.0, beta=1.0,
+                      uplo="lower", desc="DSYRK N=16384 K=8192 lower, tile 1024 (configs[2])"),
+    "cfg3_syr2k": dict(kind="syr2k", m=16384, n=16384, k=8192, tile=1024, alpha=1.0, beta=1.0,
+                       uplo="lower", desc="DSYR2K N=16384 K=8192 lower, tile 1024 (configs[2])"),
+    "cfg4_trsm": dict(kind="trsm", m=16384, n=16384, k=16384, tile=1024, alpha=1.0, beta=0.0,
+                      uplo="lower", desc="DTRSM left/lower/notrans 16384, tile 1024 (configs[3])"),
+    "cfg4_trmm": dict(kind="trmm", m=16384, n=16384, k=16384, tile=1024, alpha=1.0, beta=0.0,
+                      uplo="lower", desc="DTRMM left/lower/notrans 16384, tile 1024 (configs[3])"),
+}
+METRIC = "DGEMM TFLOP/s at 1/2/4/8 B200 (host-resident operands), % of FP64 peak"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", ",".join(str(g) for g in range(self.gpus))],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                clk, cmax = float(f[1]), float(f[2])
+            except ValueError:
+                continue
+            mx.append(cmax)
+            if clk > 0.5 * cmax:   # under load
+                sm.append(clk)
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.lines)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def make_operands(cfg, seed=0):
+    from paper_1510_05041_b200.operands import build_call
+    kw = {}
+    if "uplo" in cfg:
+        kw["uplo"] = cfg["uplo"]
+    return build_call(cfg["kind"], m=cfg["m"], n=cfg["n"], k=cfg["k"], tile_size=cfg["tile"],
+                      seed=seed, alpha=cfg["alpha"], beta=cfg["beta"],
+                      trsm_scaled=cfg["kind"] in ("trsm", "trmm"), **kw)
+
+
+def cpu_sample(cfg, call, target_s=12.0):
+    """Oracle port of the reference tiled runtime (routines.py:482-492 execute_task_on_host)
+    on sampled output tiles of the same workload, all host threads (OpenBLAS)."""
+    from oracle import tiled
+    a, b, c = (x.matrix.as_2d() for x in (call.a, call.b, call.c))
+    t = cfg["tile"]
+    kt = -(-cfg["k"] // t)
+    tiles = []
+    rng = np.random.default_rng(1)
+    nt = -(-cfg["m"] // t)
+    flops_per_tile = 2 * t * t * cfg["k"]
+    # warm-up one tile (OpenBLAS init), then as many tiles as fit target_s
+    tiled.run_tiles_subset("gemm", a, c, b, tile_size=t, tiles=[(0, 0)], alpha=cfg["alpha"],
+                           beta=cfg["beta"])
+    t0 = time.perf_counter()
+    done = 0
+    while time.perf_counter() - t0 < target_s:
+        ij = (int(rng.integers(0, nt)), int(rng.integers(0, nt)))
+        tiled.run_tiles_subset("gemm", a, c, b, tile_size=t, tiles=[ij], alpha=cfg["alpha"],
+                               beta=cfg["beta"])
+        tiles.append(ij)
+        done += 1
+    dt = time.perf_counter() - t0
+    return dict(value=done * flops_per_tile / dt / 1e12, unit="TFLOP/s", cores=os.cpu_count(),
+                kind="port", seconds=dt,
+                sample=f"{done} sampled {t}x{t} output tiles x {kt} k-steps of {cfg['desc']} "
+                       f"({done * flops_per_tile / 1e9:.0f} GFLOP), oracle/tiled.py numpy+OpenBLAS")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+
+
+def maybe_init_dist():
+    rank, world = dist_env()
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+# ----------------------------------------------------------------------------- legs
+
+def run_reference(args, cfg):
+    call = make_operands(CONFIGS["cfg2"] if cfg["kind"] != "gemm" else cfg, seed=0)
+    cfg_g = cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(cfg_g, call, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    sec = statistics.median([r["seconds"] for r in vals])
+    return {"metric": METRIC, "value": v, "unit": "TFLOP/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1))",
+            "config": {"workload": cfg_g["desc"], "m": cfg_g["m"], "n": cfg_g["n"], "k": cfg_g["k"],
+                       "tile": cfg_g["tile"]},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": vals[0]["cores"],
+                             "kind": "port", "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def device_value_leg(args, cfg, eng, lib, N):
+    """Device-resident DGEMM of the same shape, sharded by column panels over the GPUs."""
+    from paper_1510_05041_b200 import _native as NN
+    m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    ngpu = args.gpus
+    cols = [n // ngpu + (1 if g < n % ngpu else 0) for g in range(ngpu)]
+    bufs = []
+    for g in range(ngpu):
+        slot = eng.slot(g)
+        ptrs = []
+        for nelem in (m * k, k * cols[g], m * cols[g]):
+            p = C.c_uint64()
+            NN.check(lib.bx_dev_alloc(slot, nelem * 8, C.byref(p)), "alloc")
+            NN.check(lib.bx_dev_fill_uniform(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
+            ptrs.append(p.value)
+        bufs.append(ptrs)
+    for g in range(ngpu):
+        eng.device_sync(eng.slot(g))
+
+    def launch(g):
+        s = eng.slot(g)
+        a, b, c = bufs[g]
+        NN.check(lib.bx_dgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
+
+    for _ in range(args.warmup):
+        for g in range(ngpu):
+            launch(g)
+    for g in range(ngpu):
+        eng.device_sync(eng.slot(g))
+    per_launch = []
+    evs = []
+    n0 = eng.launches()
+    t_steps = []
+    for _ in range(args.steps):
+        pairs = []
+        for g in range(ngpu):
+            s = eng.slot(g)
+            e0 = eng.record(s, 0, timing=True)
+            launch(g)
+            e1 = eng.record(s, 0, timing=True)
+            pairs.append((s, e0, e1))
+        step_ms = 0.0
+        for s, e0, e1 in pairs:
+            eng.sync(e1)
+            ms = eng.elapsed_ms(e0, e1)
+            per_launch.append((ms, 2.0 * m * cols[s] * k))
+            step_ms = max(step_ms, ms)
+            eng.release(e0)
+            eng.release(e1)
+        t_steps.append(step_ms)
+    launches = eng.launches() - n0
+    for g in range(ngpu):
+        s = eng.slot(g)
+        for p in bufs[g]:
+            lib.bx_dev_free(s, p)
+    ms_step = statistics.mean(t_steps)
+    flops = 2.0 * m * n * k
+    avg_launch_ms = statistics.mean(x[0] for x in per_launch)
+    avg_launch_flops = statistics.mean(x[1] for x in per_launch)
+    return dict(value=flops / (ms_step / 1e3) / 1e12, ms_per_step=ms_step, launches=launches,
+                kernel_tflops=avg_launch_flops / (avg_launch_ms / 1e3) / 1e12,
+                avg_launch_ms=avg_launch_ms, flops_per_launch=avg_launch_flops)
+
+
+def e2e_leg(args, cfg, eng):
+    from paper_1510_05041_b200 import RunOptions, run_call
+    from paper_1510_05041_b200.devices import DeviceDesc, Topology
+    call = make_operands(cfg, seed=0)
+    topo = Topology([DeviceDesc(g, peer_group="nvlink") for g in range(args.gpus)])
+    opts = RunOptions(chunk_steps=args.chunk)
+    for m in (call.a, call.b, call.c):
+        if m is not None:
+            eng.register_host(m.matrix.storage)   # page-locking excluded from timing
+    res = None
+    for _ in range(args.warmup):
+        res = run_call(call, topo, opts)
+    times, metrics = [], []
+    n0 = eng.launches()
+    for _ in range(args.steps):
+        e0 = eng.record(0, 0, timing=True)
+        res = run_call(call, topo, opts)
+        e1 = eng.record(0, 0, timing=True)
+        eng.sync(e1)
+        times.append(eng.elapsed_ms(e0, e1))
+        eng.release(e0)
+        eng.release(e1)
+        metrics.append(res.metrics)
+    launches = eng.launches() - n0
+    ms = statistics.mean(times)
+    flops = res.plan.total_flops
+    mt = metrics[-1]
+    return dict(value=flops / (ms / 1e3) / 1e12, ms=ms, flops=flops, launches=launches,
+                h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(), p2p=mt.total_d2d_bytes(),
+                l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
+                per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
+                            for d, v in mt.devices.items()}, call=call)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--chunk", type=int, default=8)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank, world = dist_env()
+    dist = maybe_init_dist()
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        if dist:
+            dist.barrier()
+        return
+
+    if rank != 0:
+        dist.barrier()   # start
+        dist.barrier()   # end
+        return
+
+    from paper_1510_05041_b200 import _native as NN
+    from paper_1510_05041_b200.engine import get_engine
+    lib = NN.load()
+    NN.require_gpu()
+    eng = get_engine(list(range(args.gpus)), 4)
+    peak = C.c_double()
+    NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
+    if dist:
+        dist.barrier()
+
+    with ClockSampler(args.gpus) as clk:
+        if cfg["kind"] == "gemm":
+            val = device_value_leg(args, cfg, eng, lib, NN)
+        else:
+            val = None
+        e2e = e2e_leg(args, cfg, eng)
+    if dist:
+        dist.barrier()
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"],
+                         e2e["call"] if cfg["kind"] == "gemm" else make_operands(CONFIGS["cfg2"]),
+                         target_s=10.0)
+
+    flops = e2e["flops"]
+    h2d_bw, p2p_bw = 53.0e9, 700e9      # measured (profiles/peaks_r01.json); P2P: nominal-measured
+    t_a = flops / (args.gpus * peak.value * 1e12)
+    t_b = e2e["h2d"] / (h2d_bw * args.gpus) + e2e["p2p"] / (p2p_bw * args.gpus)
+    prof = os.path.join(ROOT, "profiles", "ncu_dgemm_traffic_r01.json")
+    traffic = None
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    kernel_tf = val["kernel_tflops"] if val else e2e["value"]
+    out = {
+        "metric": METRIC,
+        "value": val["value"] if val else e2e["value"],
+        "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": val["ms_per_step"] if val else e2e["ms"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: seeded uniform[-1,1) (reference build_call generator) for e2e; "
+                "device-filled uniform[-1,1) for the HBM-resident leg",
+        "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
+                   "tile": cfg["tile"], "alpha": cfg["alpha"], "beta": cfg["beta"],
+                   "l2_flush": "none needed: every step streams > 6 GiB of operands through a 126 MB L2",
+                   "chunk_steps": args.chunk},
+        "e2e": {"value": e2e["value"], "unit": "TFLOP/s", "ms_per_step": e2e["ms"],
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                "p2p_bytes_per_step": e2e["p2p"],
+                "frac_of_fp64_peak": e2e["value"] / (args.gpus * peak.value),
+                "cache": {"l1_hits": e2e["l1"], "l2_hits": e2e["l2"], "host_fetches": e2e["host"]},
+                "per_device": e2e["per_device"],
+                "roofline_north_star": {"t_tensor_s": t_a, "t_link_s": t_b,
+                                        "frac": max(t_a, t_b) / (e2e["ms"] / 1e3),
+                                        "h2d_gbs_assumed": h2d_bw / 1e9, "p2p_gbs_assumed": p2p_bw / 1e9}},
+        "roofline": {"bound": "tensor", "achieved": kernel_tf, "peak": peak.value, "unit": "TFLOP/s",
+                     "frac": kernel_tf / peak.value, "traffic": traffic,
+                     "kernel": "bx::gemm_task_kernel (FP64 DMMA m8n8k4)",
+                     "peak_source": "measured live: register-only DMMA.8x8x4 loop (bx_fp64_peak_probe); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "flops_per_launch": val["flops_per_launch"] if val else None,
+                     "avg_launch_ms": val["avg_launch_ms"] if val else None},
+        "gpu_launches": e2e["launches"] + (val["launches"] if val else 0),
+        "gpu_launches_e2e": e2e["launches"],
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

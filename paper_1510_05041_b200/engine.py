@@ -1,0 +1,210 @@
+"""The CUDA tile engine seen from the host runtime (a thin object over the C ABI).
+
+One process-wide engine owns the per-GPU state created by ``bx_init`` (arena reservation,
+4 compute streams + H2D / D2H / P2P copy streams, event pool).  The scheduler talks to it
+through the methods below; tests substitute a fake with the same surface.  There is no
+CPU implementation of any of these operations.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+from . import _native as N
+
+LANE_H2D, LANE_D2H, LANE_P2P = N.LANE_H2D, N.LANE_D2H, N.LANE_P2P
+
+
+class CudaEngine:
+    kind = "cuda"
+
+    def __init__(self, cuda_ids, n_compute: int = 4):
+        self.lib = N.load()
+        N.require_gpu()
+        self.cuda_ids = list(cuda_ids)
+        self.n_compute = n_compute
+        self._arena = [0] * len(self.cuda_ids)
+        self._lock = threading.Lock()
+        N.check(self.lib.bx_init(len(self.cuda_ids), N.int_array(self.cuda_ids), None, n_compute),
+                "bx_init")
+
+    # ---- devices / memory -------------------------------------------------------------
+
+    def slot(self, cuda_id: int) -> int:
+        return self.cuda_ids.index(cuda_id)
+
+    def extend(self, more_ids, n_compute) -> None:
+        ids = self.cuda_ids + [d for d in more_ids if d not in self.cuda_ids]
+        n_compute = max(n_compute, self.n_compute)
+        N.check(self.lib.bx_init(len(ids), N.int_array(ids), None, n_compute), "bx_init")
+        self._arena += [0] * (len(ids) - len(self.cuda_ids))
+        self.cuda_ids, self.n_compute = ids, n_compute
+
+    @property
+    def ndev(self) -> int:
+        return len(self.cuda_ids)
+
+    def device_info(self, slot: int) -> dict:
+        name = C.create_string_buffer(128)
+        sms, tot, free = C.c_int(), C.c_uint64(), C.c_uint64()
+        N.check(self.lib.bx_device_info(self.cuda_ids[slot], name, 128, C.byref(sms),
+                                        C.byref(tot), C.byref(free)), "device_info")
+        return dict(name=name.value.decode(), sms=sms.value, total_bytes=tot.value,
+                    free_bytes=free.value)
+
+    def ensure_arenas(self, capacities: dict) -> None:
+        """Grow-only per-device reservations (one cudaMalloc each); {slot: bytes}."""
+        need = [max(int(capacities.get(i, 0)), cur) for i, cur in enumerate(self._arena)]
+        if need == self._arena:
+            return
+        N.check(self.lib.bx_init(self.ndev, N.int_array(self.cuda_ids), N.u64_array(need),
+                                 self.n_compute), "arena reservation")
+        self._arena = need
+
+    def arena_capacity(self, slot: int) -> int:
+        return self._arena[slot]
+
+    def register_host(self, array) -> bool:
+        """Page-lock a host buffer; returns True if this call registered it (the caller
+        then owns the matching ``unregister_host``)."""
+        yes = C.c_int(0)
+        self.lib.bx_host_is_registered(C.c_void_p(array.ctypes.data), C.byref(yes))
+        if yes.value:
+            return False
+        N.check(self.lib.bx_host_register(C.c_void_p(array.ctypes.data), array.nbytes),
+                "host register")
+        return True
+
+    def unregister_host(self, array) -> None:
+        N.check(self.lib.bx_host_unregister(C.c_void_p(array.ctypes.data)), "host unregister")
+
+    # ---- transfers ----------------------------------------------------------------------
+
+    @staticmethod
+    def _waits(waits):
+        if not waits:
+            return 0, None
+        return len(waits), N.int_array(waits)
+
+    def h2d(self, slot, dst_off, dst_ld, desc, r0, c0, h, w, waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_h2d_tile(slot, dst_off, dst_ld, C.c_void_p(desc.element_address(r0, c0)),
+                                     desc.leading_dim, h, w, desc.itemsize, nw, wp, C.byref(ev)),
+                "h2d tile")
+        return ev.value
+
+    def d2h(self, slot, src_off, src_ld, desc, r0, c0, h, w, waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_d2h_tile(slot, src_off, src_ld, C.c_void_p(desc.element_address(r0, c0)),
+                                     desc.leading_dim, h, w, desc.itemsize, nw, wp, C.byref(ev)),
+                "d2h tile")
+        return ev.value
+
+    def p2p(self, dst_slot, dst_off, src_slot, src_off, nbytes, waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_p2p_tile(dst_slot, dst_off, src_slot, src_off, nbytes, nw, wp,
+                                     C.byref(ev)), "p2p tile")
+        return ev.value
+
+    # ---- kernels ------------------------------------------------------------------------
+
+    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=()) -> int:
+        n = len(steps)
+        a_off = (C.c_uint64 * n)(*[s[0] for s in steps])
+        lda = (C.c_int * n)(*[s[1] for s in steps])
+        b_off = (C.c_uint64 * n)(*[s[2] for s in steps])
+        ldb = (C.c_int * n)(*[s[3] for s in steps])
+        dep = (C.c_int * n)(*[s[4] for s in steps])
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_gemm_task(slot, stream, int(ta), int(tb), tri, h, w, n, a_off, lda,
+                                      b_off, ldb, dep, float(alpha), float(beta), c_off, ldc,
+                                      nw, wp, C.byref(ev)), "gemm task")
+        return ev.value
+
+    def trsm(self, slot, stream, right, upper, trans, unit, h, w, alpha, a_off, lda, b_off, ldb,
+             waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_trsm_tile(slot, stream, int(right), int(upper), int(trans), int(unit),
+                                      h, w, float(alpha), a_off, lda, b_off, ldb, nw, wp,
+                                      C.byref(ev)), "trsm tile")
+        return ev.value
+
+    def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
+                    waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_materialize(slot, stream, int(mode_sym), int(upper), int(trans),
+                                        int(unit), n, a_off, lda, dst_off, ldd, nw, wp, C.byref(ev)),
+                "materialize")
+        return ev.value
+
+    def singular(self, slot, reset=True) -> bool:
+        f = C.c_int(0)
+        N.check(self.lib.bx_singular_flag(slot, int(reset), C.byref(f)))
+        return bool(f.value)
+
+    # ---- events -------------------------------------------------------------------------
+
+    def record(self, slot, lane, timing=False) -> int:
+        ev = C.c_int(-1)
+        N.check(self.lib.bx_event_record(slot, lane, int(timing), C.byref(ev)), "event record")
+        return ev.value
+
+    def done(self, ev) -> bool:
+        rc = self.lib.bx_event_query(ev)
+        if rc < 0 or rc > 1:
+            N.check(rc, "event query")
+        return rc == 0
+
+    def wait_any(self, evs, spin_us=-1) -> int:
+        idx = C.c_int(-1)
+        N.check(self.lib.bx_event_wait_any(len(evs), N.int_array(evs), C.byref(idx), spin_us),
+                "wait_any")
+        return idx.value
+
+    def sync(self, ev) -> None:
+        N.check(self.lib.bx_event_sync(ev), "event sync")
+
+    def elapsed_ms(self, ev0, ev1) -> float:
+        ms = C.c_float(0.0)
+        N.check(self.lib.bx_event_elapsed(ev0, ev1, C.byref(ms)), "event elapsed")
+        return ms.value
+
+    def release(self, ev) -> None:
+        if ev is not None and ev >= 0:
+            self.lib.bx_event_release(ev)
+
+    def stream_wait(self, slot, lane, ev) -> None:
+        N.check(self.lib.bx_stream_wait(slot, lane, ev), "stream wait")
+
+    def device_sync(self, slot) -> None:
+        N.check(self.lib.bx_device_sync(slot), "device sync")
+
+    def launches(self) -> int:
+        n = C.c_uint64(0)
+        self.lib.bx_launch_count(C.byref(n))
+        return n.value
+
+
+_ENGINE = None
+_ELOCK = threading.Lock()
+
+
+def get_engine(cuda_ids, n_compute=4) -> CudaEngine:
+    """The process-wide engine, extended to cover ``cuda_ids``.  Engine slots are
+    positions in its device list; use ``engine.slot(cuda_id)``."""
+    global _ENGINE
+    with _ELOCK:
+        if _ENGINE is None:
+            _ENGINE = CudaEngine(list(cuda_ids), n_compute)
+            return _ENGINE
+        missing = [d for d in cuda_ids if d not in _ENGINE.cuda_ids]
+        if missing or n_compute > _ENGINE.n_compute:
+            _ENGINE.extend(missing, n_compute)
+        return _ENGINE

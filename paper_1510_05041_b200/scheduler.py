@@ -1,0 +1,760 @@
+"""BLASX runtime on real GPUs: demand-driven work sharing, per-GPU reservation stations
+with locality priorities and work stealing, whole-task issue onto 4 CUDA streams per GPU,
+a two-level tile cache, and event-driven completion.
+
+Scheduling policy = the reference's (/root/reference/pkg/src/tileblas/scheduler.py):
+  * ready tasks sit in one global FIFO (TaskQueue, scheduler.py:55-77);
+  * each GPU keeps a reservation station of up to ``rs_capacity`` pending tasks, refilled
+    from the FIFO; only a GPU whose queue pull and station both come up empty steals,
+    taking the lowest-priority task of the station with the most pending tasks, and only
+    from stations holding >= 2 (scheduler.py:297-318, 542-558, 140-149);
+  * a task's priority counts +2 per input tile already in this GPU's L1 and +1 per tile
+    held by a peer (Eq. 3, scheduler.py:341-354); the best pending task (ties -> lowest id)
+    runs next;
+  * up to 4 tasks run concurrently per GPU, one per compute stream (devices.py:36).
+
+What is different on hardware (SURVEY.md §7 "hard parts" 3-4):
+  * a task is issued *whole*: its tile translations (L1 hit / P2P copy from a peer / H2D
+    copy from pinned host memory) and its kernels are enqueued in one pass, the kernels
+    waiting on the copies' CUDA events; consecutive k-steps are fused into one kernel
+    launch (``chunk_steps``) so C stays in registers across them;
+  * C is written back with a D2H copy ordered after the last kernel; the task completes
+    when that copy's event fires — only then are its reader pins released, its buffers
+    freed and TRSM dependents enqueued (readiness tied to write-back);
+  * pressure sync (every cached tile pinned) = flush + drain this GPU + release the pins of
+    all launched work, then retry once (cache.py:232-250; scheduler.py:272-281).
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from collections import deque
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .cache import HOST_FETCH, L1_HIT, L2_HIT, CoherenceDirectory, DeviceTileCache
+from .devices import (DeviceMetrics, Metrics, Topology, TraceEvent, discover_topology,
+                      exposed_comm_time)
+from .errors import CapacityDeadlockError, ConfigError, SingularMatrixError
+from .memory import Arena
+from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
+                       TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
+from .tiling import device_ld
+
+WORKING_SET_TILES = 12   # reference floor (scheduler.py:49-52): 4 tasks x (C + 2 inputs)
+LANE_H2D, LANE_D2H, LANE_P2P = -1, -2, -3
+
+
+class TaskQueue:
+    """Global FIFO of ready task ids (append / popleft are atomic)."""
+
+    def __init__(self):
+        self._items = deque()
+
+    def put(self, item) -> None:
+        self._items.append(item)
+
+    def get(self):
+        try:
+            return self._items.popleft()
+        except IndexError:
+            return None
+
+    def __len__(self) -> int:
+        return len(self._items)
+
+
+@dataclass
+class RunOptions:
+    execution: str = "deterministic"   # one driver thread; "concurrent": one per GPU
+    rs_capacity: int = 8
+    l1_enabled: bool = True
+    l2_enabled: bool = True
+    record_trace: bool = False
+    n_streams: int = 4
+    chunk_steps: int = 8               # k-steps fused per kernel launch
+    arena_bytes: int = 0               # per GPU; 0 = sized for the call
+
+
+@dataclass
+class RunResult:
+    metrics: Metrics
+    trace: list
+    tasks_by_device: dict
+    plan: TaskPlan
+
+
+class _SlotEntry:
+    __slots__ = ("task", "release_time", "priority")
+
+    def __init__(self, task: Task, release_time: float = 0.0):
+        self.task = task
+        self.release_time = release_time
+        self.priority = 0
+
+
+class ReservationStation:
+    """Per-GPU buffer of upcoming tasks, open to theft (scheduler.py:106-153)."""
+
+    def __init__(self, device_id: int, capacity: int):
+        self.device_id = device_id
+        self.capacity = capacity
+        self.lock = threading.Lock()
+        self._pending = []
+
+    def pending_count(self) -> int:
+        with self.lock:
+            return len(self._pending)
+
+    def room(self, in_flight: int = 0) -> int:
+        with self.lock:
+            return self.capacity - in_flight - len(self._pending)
+
+    def put(self, entry) -> None:
+        with self.lock:
+            self._pending.append(entry)
+
+    def pop_best(self):
+        with self.lock:
+            if not self._pending:
+                return None
+            best = min(self._pending, key=lambda e: (-e.priority, e.task.task_id))
+            self._pending.remove(best)
+            return best
+
+    def steal_lowest(self):
+        with self.lock:
+            if len(self._pending) < 2:
+                return None
+            worst = min(self._pending, key=lambda e: (e.priority, e.task.task_id))
+            self._pending.remove(worst)
+            return worst
+
+    def entries(self) -> list:
+        with self.lock:
+            return list(self._pending)
+
+
+def steal_for(thief):
+    """Victim = most pending (ties: lowest device id); it gives up its lowest-priority
+    task; never robs a station with < 2 pending; only when the global queue is empty."""
+    if len(thief.runtime.queue) > 0:
+        return None
+    victims = sorted((w for w in thief.runtime.workers if w.device_id != thief.device_id),
+                     key=lambda w: (-w.rs.pending_count(), w.device_id))
+    for v in victims:
+        e = v.rs.steal_lowest()
+        if e is not None:
+            return e
+    return None
+
+
+class _Runtime:
+    def __init__(self, plan: TaskPlan, topology: Topology, options: RunOptions, engine):
+        self.plan = plan
+        self.topology = topology
+        self.options = options
+        self.engine = engine
+        self.queue = TaskQueue()
+        self.directory = CoherenceDirectory()
+        self.total = len(plan.tasks)
+        self._done = 0
+        self._deps = {t.task_id: t.deps_remaining for t in plan.tasks}
+        self._lock = threading.Lock()
+        self.trace = []
+        self.device_metrics = {d.device_id: DeviceMetrics() for d in topology.devices}
+        self.workers = []
+        self.error = None
+        for t in plan.tasks:
+            if t.deps_remaining == 0:
+                self.queue.put((t.task_id, 0.0))
+
+    def done(self) -> bool:
+        with self._lock:
+            return self._done >= self.total
+
+    def complete_task(self, task: Task, at_time: float = 0.0) -> None:
+        with self._lock:
+            self._done += 1
+            for dep in task.dependents:
+                self._deps[dep] -= 1
+                if self._deps[dep] == 0:
+                    self.queue.put((dep, at_time))
+
+    def add_d2d_out(self, device_id, nbytes) -> None:
+        with self._lock:
+            self.device_metrics[device_id].d2d_out_bytes += nbytes
+
+    def record(self, ev: TraceEvent) -> None:
+        with self._lock:
+            self.trace.append(ev)
+
+
+class _Chunk:
+    """Consecutive gemm sub-steps fused into one kernel launch."""
+    __slots__ = ("ta", "tb", "tri", "alpha", "beta", "steps", "waits", "k")
+
+    def __init__(self, ta, tb, tri, alpha, beta, k):
+        self.ta, self.tb, self.tri, self.alpha, self.beta, self.k = ta, tb, tri, alpha, beta, k
+        self.steps = []
+        self.waits = []
+
+
+class _Active:
+    """A task in flight on one compute stream."""
+    __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
+                 "events", "last_ev", "done_ev", "chunk", "pending_waits", "flops",
+                 "trace_evs")
+
+    def __init__(self, entry, stream):
+        self.entry = entry
+        self.stream = stream
+        self.c_off = -1
+        self.c_ld = 0
+        self.scratch = []        # arena offsets freed at retirement
+        self.pins = []           # (cache, block) pinned for the not-yet-launched chunk
+        self.launched_pins = []  # pins of launched chunks (releasable after a drain)
+        self.events = []         # event ids owned by the task
+        self.last_ev = None      # event after the last kernel
+        self.done_ev = None      # write-back completion
+        self.chunk = None
+        self.pending_waits = []  # waits to attach to the next launch (C move-in)
+        self.flops = 0
+        self.trace_evs = []      # (kind, lane, ev0, ev1, nbytes_or_flops, k)
+
+
+class _GpuWorker:
+    """One GPU: reservation station, L1 cache over its arena, 4 stream slots; also the
+    ``fetch`` object of its cache's translate protocol."""
+
+    def __init__(self, desc, runtime: _Runtime):
+        self.desc = desc
+        self.device_id = desc.device_id
+        self.runtime = runtime
+        self.eng = runtime.engine
+        self.slot = self.eng.slot(desc.device_id)
+        opts = runtime.options
+        self.arena = Arena(self.eng.arena_capacity(self.slot))
+        self.cache = DeviceTileCache(desc.device_id, self.arena, runtime.directory,
+                                     peer_group=runtime.topology.peer_group_of(desc),
+                                     l2_enabled=opts.l2_enabled, on_evict=self._on_evict)
+        self.rs = ReservationStation(desc.device_id, opts.rs_capacity)
+        self.dm = runtime.device_metrics[desc.device_id]
+        self.active = [None] * opts.n_streams
+        self.l1_hits = self.l2_hits = self.host_fetches = 0
+        self.tasks_done = 0
+        self._cur: Optional[_Active] = None
+        self.plan = runtime.plan
+        self.esz = runtime.plan.dtype.itemsize
+        self.tile = runtime.plan.tile_size
+        self.trace_on = opts.record_trace
+        self.epoch = None
+
+    # ---- cache callbacks ------------------------------------------------------------
+
+    def _on_evict(self, blk) -> None:
+        if blk.ready_ev is not None:
+            self.eng.release(blk.ready_ev)
+            blk.ready_ev = None
+
+    def _tile_geom(self, ref):
+        h, w = ref.phys_height, ref.phys_width
+        ld = device_ld(h)
+        return h, w, ld, ld * w * self.esz
+
+    def _host_of(self, ref):
+        return self.plan.matrices[ref.matrix_id], ref.i * self.tile, ref.j * self.tile
+
+    def _timed(self, lane, op, waits, kind, amount, k=-1):
+        """Run ``op(waits)``; in trace mode bracket it with timing events."""
+        if not self.trace_on:
+            return op(waits)
+        for w in waits:
+            self.eng.stream_wait(self.slot, lane, w)
+        e0 = self.eng.record(self.slot, lane, timing=True)
+        ev = op(())
+        e1 = self.eng.record(self.slot, lane, timing=True)
+        task_id = self._cur.entry.task.task_id if self._cur is not None else -1
+        self.runtime_trace.append((kind, lane, e0, e1, amount, task_id, k))
+        return ev
+
+    def copy_from_host(self, ref, blk) -> None:
+        desc, r0, c0 = self._host_of(ref)
+        h, w, ld, _ = self._tile_geom(ref)
+        blk.ld = ld
+        blk.ready_ev = self._timed(
+            LANE_H2D, lambda wt: self.eng.h2d(self.slot, blk.offset, ld, desc, r0, c0, h, w, wt),
+            (), "H2D", h * w * self.esz)
+        self.dm.h2d_bytes += h * w * self.esz
+
+    def copy_from_peer(self, src_cache, src_blk, ref, blk) -> bool:
+        h, w, ld, nbytes = self._tile_geom(ref)
+        blk.ld = ld
+        waits = []
+        if src_blk.ready_ev is not None and not src_blk.ready_done:
+            if self.eng.done(src_blk.ready_ev):
+                src_blk.ready_done = True
+            else:
+                waits.append(src_blk.ready_ev)
+        src_slot = self.eng.slot(src_cache.device_id)
+        blk.ready_ev = self._timed(
+            LANE_P2P, lambda wt: self.eng.p2p(self.slot, blk.offset, src_slot, src_blk.offset,
+                                              nbytes, wt), waits, "D2D", h * w * self.esz)
+        self.dm.d2d_in_bytes += h * w * self.esz
+        self.runtime.add_d2d_out(src_cache.device_id, h * w * self.esz)
+        # the source stays pinned until the consumer task completes
+        self._cur.pins.append((src_cache, src_blk))
+        return True
+
+    def pressure_sync(self) -> None:
+        """Every cached block is pinned: launch what is pending, drain the GPU, release the
+        pins of all launched work and retire finished tasks, then let the caller retry."""
+        cur = self._cur
+        if cur is not None and cur.chunk is not None:
+            self._flush(cur)
+        self.eng.device_sync(self.slot)
+        for act in [a for a in self.active if a is not None] + ([cur] if cur else []):
+            for cache, blk in act.launched_pins:
+                cache.unpin(blk)
+            act.launched_pins = []
+        self._retire_finished(block=False)
+        if self.trace_on:
+            t = self._now()
+            self.runtime.record(TraceEvent(t, t, self.device_id, -1, "SYNC", 0, -1, -1))
+
+    def _now(self) -> float:
+        e = self.eng.record(self.slot, 0, timing=True)
+        self.eng.sync(e)
+        t = self.eng.elapsed_ms(self.epoch, e) / 1e3
+        self.eng.release(e)
+        return t
+
+    # ---- scheduling -----------------------------------------------------------------
+
+    def _refill(self) -> None:
+        while self.rs.room(0) > 0:
+            item = self.runtime.queue.get()
+            if item is None:
+                break
+            self.rs.put(_SlotEntry(self.plan.tasks[item[0]], item[1]))
+        if self.rs.pending_count() == 0:
+            stolen = steal_for(self)
+            if stolen is not None:
+                self.rs.put(stolen)
+
+    def _priority(self, task: Task) -> int:
+        contains = self.cache.contains
+        peer = self.runtime.directory.peer_source
+        l2 = self.runtime.options.l2_enabled
+        p = 0
+        for step in task.steps:
+            for ref in step.input_refs():
+                key = ref.key()
+                if contains(key):
+                    p += 2
+                elif l2 and peer(key, self.device_id) is not None:
+                    p += 1
+        return p
+
+    def _next_entry(self):
+        self._refill()
+        for e in self.rs.entries():
+            e.priority = self._priority(e.task)
+        return self.rs.pop_best()
+
+    def fill(self) -> bool:
+        issued = False
+        for s, act in enumerate(self.active):
+            if act is not None:
+                continue
+            entry = self._next_entry()
+            if entry is None:
+                break
+            self._issue(entry, s)
+            issued = True
+        return issued
+
+    # ---- issue ----------------------------------------------------------------------
+
+    def _resolve(self, ref):
+        """Translate + pin one input tile; returns (offset, ld, arrival-wait or None)."""
+        act = self._cur
+        h, w, ld, nbytes = self._tile_geom(ref)
+        if not self.runtime.options.l1_enabled:
+            off = self.cache.allocate_under_pressure(nbytes, self)
+            act.scratch.append(off)
+            desc, r0, c0 = self._host_of(ref)
+            ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(self.slot, off, ld, desc, r0, c0,
+                                                               h, w, wt), (), "H2D", h * w * self.esz)
+            act.events.append(ev)
+            self.dm.h2d_bytes += h * w * self.esz
+            self.host_fetches += 1
+            return off, ld, ev
+        blk, outcome = self.cache.translate(ref, self, nbytes=nbytes, ld=ld)
+        if outcome == L1_HIT:
+            self.l1_hits += 1
+        elif outcome == L2_HIT:
+            self.l2_hits += 1
+        else:
+            self.host_fetches += 1
+        self.cache.pin(blk)
+        act.pins.append((self.cache, blk))
+        wait = None
+        if blk.ready_ev is not None and not blk.ready_done:
+            if self.eng.done(blk.ready_ev):
+                blk.ready_done = True
+            else:
+                wait = blk.ready_ev
+        return blk.offset, blk.ld, wait
+
+    def _add_sub(self, act, ta, tb, tri, alpha, beta, a, b, depth, k):
+        ch = act.chunk
+        max_steps = self.runtime.options.chunk_steps
+        if (ch is None or (ch.ta, ch.tb, ch.tri, ch.alpha) != (ta, tb, tri, alpha)
+                or beta != 1.0 or len(ch.steps) >= max_steps):
+            if ch is not None:
+                self._flush(act)
+            ch = act.chunk = _Chunk(ta, tb, tri, alpha, beta, k)
+        ch.steps.append((a[0], a[1], b[0], b[1], depth))
+        for wv in (a[2], b[2]):
+            if wv is not None and wv not in ch.waits:
+                ch.waits.append(wv)
+
+    def _flush(self, act) -> None:
+        ch = act.chunk
+        if ch is None:
+            return
+        act.chunk = None
+        task = act.entry.task
+        h, w = task.out_ref.phys_height, task.out_ref.phys_width
+        waits = ch.waits + act.pending_waits
+        act.pending_waits = []
+        flops = sum(2 * h * w * s[4] for s in ch.steps)
+        ev = self._timed(act.stream, lambda wt: self.eng.gemm(
+            self.slot, act.stream, ch.ta, ch.tb, ch.tri, h, w, ch.steps, ch.alpha, ch.beta,
+            act.c_off, act.c_ld, wt), waits, "KERNEL", flops, ch.k)
+        self._launched(act, ev)
+
+    def _launched(self, act, ev) -> None:
+        act.events.append(ev)
+        act.last_ev = ev
+        act.launched_pins.extend(act.pins)
+        act.pins = []
+        self.dm.kernel_launches += 1
+
+    def _scratch_tile(self, act, n):
+        ld = device_ld(n)
+        off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
+        act.scratch.append(off)
+        return off, ld
+
+    def _issue(self, entry, stream) -> None:
+        task = entry.task
+        call = self.plan.call
+        act = _Active(entry, stream)
+        self._cur = act
+        try:
+            out = task.out_ref
+            h, w = out.phys_height, out.phys_width
+            act.c_ld = device_ld(h)
+            act.c_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
+            if task.needs_c_move_in:
+                desc, r0, c0 = self._host_of(out)
+                ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(
+                    self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
+                    h * w * self.esz)
+                act.events.append(ev)
+                act.pending_waits.append(ev)
+                self.dm.h2d_bytes += h * w * self.esz
+            tri_mode = 1 if call.uplo == "lower" else 2
+            for st in task.steps:
+                kind = st.kind
+                if kind == GEMM_UPDATE:
+                    a = self._resolve(st.a)
+                    b = self._resolve(st.b)
+                    self._add_sub(act, st.a.transposed, st.b.transposed, 0, st.alpha, st.beta,
+                                  a, b, st.a.width, st.k)
+                elif kind == SYRK_UPDATE:
+                    a = self._resolve(st.a)
+                    self._add_sub(act, st.a.transposed, not st.a.transposed, tri_mode, st.alpha,
+                                  st.beta, a, a, st.a.width, st.k)
+                elif kind == SYR2K_UPDATE:
+                    a = self._resolve(st.a)
+                    b = self._resolve(st.b)
+                    self._add_sub(act, st.a.transposed, not st.b.transposed, tri_mode, st.alpha,
+                                  st.beta, a, b, st.a.width, st.k)
+                    self._add_sub(act, st.b.transposed, not st.a.transposed, tri_mode, st.alpha,
+                                  1.0, b, a, st.a.width, st.k)
+                elif kind in (TRMM_DIAG, SYMM_DIAG):
+                    a = self._resolve(st.a)
+                    b = self._resolve(st.b)
+                    n = st.a.phys_height
+                    s_off, s_ld = self._scratch_tile(act, n)
+                    sym = kind == SYMM_DIAG
+                    waits = [a[2]] if a[2] is not None else []
+                    ev = self._timed(stream, lambda wt: self.eng.materialize(
+                        self.slot, stream, sym, call.uplo == "upper",
+                        False if sym else call.trans_a, (not sym) and call.diag == "unit", n,
+                        a[0], a[1], s_off, s_ld, wt), waits, "KERNEL", 0, st.k)
+                    act.events.append(ev)
+                    scratch = (s_off, s_ld, None)
+                    if call.side == "left":
+                        self._add_sub(act, False, st.b.transposed, 0, st.alpha, st.beta,
+                                      scratch, b, n, st.k)
+                    else:
+                        self._add_sub(act, st.b.transposed, False, 0, st.alpha, st.beta,
+                                      b, scratch, n, st.k)
+                elif kind == TRSM_SOLVE:
+                    a = self._resolve(st.a)
+                    self._flush(act)
+                    waits = ([a[2]] if a[2] is not None else []) + act.pending_waits
+                    act.pending_waits = []
+                    flops = st.flops
+                    ev = self._timed(stream, lambda wt: self.eng.trsm(
+                        self.slot, stream, call.side == "right", call.uplo == "upper",
+                        call.trans_a, call.diag == "unit", h, w, st.alpha, a[0], a[1],
+                        act.c_off, act.c_ld, wt), waits, "KERNEL", flops, st.k)
+                    self._launched(act, ev)
+                else:
+                    raise ConfigError(f"unknown step kind {kind!r}")
+            self._flush(act)
+            desc, r0, c0 = self._host_of(out)
+            waits = [act.last_ev] + act.pending_waits
+            act.pending_waits = []
+            act.done_ev = self._timed(LANE_D2H, lambda wt: self.eng.d2h(
+                self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), waits, "D2H",
+                h * w * self.esz)
+            self.dm.d2h_bytes += h * w * self.esz
+            act.events.append(act.done_ev)
+            act.flops = task.flops
+        finally:
+            self._cur = None
+        self.active[stream] = act
+
+    # ---- completion -----------------------------------------------------------------
+
+    def in_flight(self) -> list:
+        return [a.done_ev for a in self.active if a is not None]
+
+    def _retire(self, act) -> None:
+        task = act.entry.task
+        for cache, blk in act.pins + act.launched_pins:
+            cache.unpin(blk)
+        act.pins = act.launched_pins = []
+        self.arena.free(act.c_off)
+        for off in act.scratch:
+            self.arena.free(off)
+        for ev in act.events:
+            self.eng.release(ev)
+        self.runtime.directory.note_write_back(task.out_ref.key())
+        if self.plan.call.kind == "trsm" and self.eng.singular(self.slot, reset=True):
+            raise SingularMatrixError("zero on a non-unit triangular diagonal")
+        self.tasks_done += 1
+        self.dm.tasks += 1
+        self.runtime.complete_task(task)
+
+    def _retire_finished(self, block: bool) -> bool:
+        got = False
+        for s, act in enumerate(self.active):
+            if act is None:
+                continue
+            if self.eng.done(act.done_ev):
+                self.active[s] = None
+                self._retire(act)
+                got = True
+        return got
+
+    def poll(self) -> bool:
+        return self._retire_finished(block=False)
+
+    def idle(self) -> bool:
+        return all(a is None for a in self.active)
+
+    def release_all(self) -> None:
+        for blk in self.cache.blocks():
+            self._on_evict(blk)
+
+
+def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: int) -> int:
+    """Enough for every distinct input tile plus the in-flight C / scratch buffers,
+    capped at 90 % of free HBM (no eviction at BASELINE sizes on a 180 GB B200)."""
+    esz = plan.dtype.itemsize
+    t = plan.tile_size
+    seen = {}
+    for task in plan.tasks:
+        for st in task.steps:
+            for ref in st.input_refs():
+                if ref.key() not in seen:
+                    seen[ref.key()] = device_ld(ref.phys_height) * ref.phys_width * esz
+    per_tile = device_ld(t) * t * esz
+    want = sum(-(-v // 256) * 256 for v in seen.values())
+    want += (options.n_streams + 2) * 2 * per_tile + (64 << 20)
+    cap = int(free_bytes * 0.9) - (1 << 30)
+    return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
+
+
+def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
+             options: Optional[RunOptions] = None, engine=None) -> RunResult:
+    """Execute a task plan on the topology's GPUs; the host output holds the result."""
+    from .engine import get_engine
+    options = options or RunOptions()
+    if options.execution not in ("deterministic", "concurrent"):
+        raise ConfigError(f"unknown execution mode {options.execution!r}")
+    if not 1 <= options.n_streams <= 8:
+        raise ConfigError("n_streams must be in 1..8")
+    if options.chunk_steps < 1:
+        raise ConfigError("chunk_steps must be >= 1")
+    topology = topology or discover_topology()
+    devs = topology.accelerators()
+    if engine is None:
+        engine = get_engine([d.device_id for d in devs], options.n_streams)
+    esz = plan.dtype.itemsize
+    per_tile = device_ld(plan.tile_size) * plan.tile_size * esz
+    caps = {}
+    for d in devs:
+        slot = engine.slot(d.device_id)
+        want = d.arena_capacity or options.arena_bytes
+        if not want:
+            want = _auto_arena_bytes(plan, options, engine.device_info(slot)["free_bytes"]
+                                     + engine.arena_capacity(slot))
+        if want <= WORKING_SET_TILES * per_tile:
+            raise ConfigError(
+                f"device {d.device_id}: arena of {want} bytes cannot hold the "
+                f"{WORKING_SET_TILES}-tile working set at tile size {plan.tile_size}")
+        caps[slot] = want
+    engine.ensure_arenas(caps)
+    # Page-lock the operands for the DMA engine.  Buffers pinned by the caller beforehand
+    # (``pin_host``; the paper excludes page-locking from timing) stay
+    # pinned; the ones pinned here are unpinned when the call returns.
+    pinned_here = [m.storage for m in plan.matrices.values() if engine.register_host(m.storage)]
+
+    rt = _Runtime(plan, topology, options, engine)
+    workers = [_GpuWorker(d, rt) for d in devs]
+    for w in workers:
+        # an explicit capacity smaller than the reservation bounds the arena (eviction tests)
+        if caps[w.slot] < w.arena.capacity:
+            w.arena = Arena(caps[w.slot])
+            w.cache.arena = w.arena
+        w.runtime_trace = []
+    rt.workers = workers
+    for w in workers:
+        w.epoch = engine.record(w.slot, 0, timing=True)
+    t0 = time.perf_counter()
+    try:
+        if options.execution == "deterministic":
+            _drive_single(rt, workers)
+        else:
+            _drive_threads(rt, workers)
+    except BaseException:
+        for w in workers:
+            try:
+                engine.device_sync(w.slot)
+            except Exception:
+                pass
+        _unpin(engine, pinned_here)
+        raise
+    wall = time.perf_counter() - t0
+    metrics = _finalize(rt, workers, wall)
+    for w in workers:
+        w.release_all()
+    _unpin(engine, pinned_here)
+    return RunResult(metrics, sorted(rt.trace, key=lambda e: (e.time_start, e.device, e.time_end)),
+                     {w.device_id: w.tasks_done for w in workers}, plan)
+
+
+def _unpin(engine, arrays) -> None:
+    for arr in arrays:
+        try:
+            engine.unregister_host(arr)
+        except Exception:
+            pass
+
+
+def _drive_single(rt: _Runtime, workers) -> None:
+    eng = rt.engine
+    while not rt.done():
+        progressed = False
+        for w in workers:
+            progressed |= w.poll()
+        for w in workers:
+            progressed |= w.fill()
+        if rt.done():
+            break
+        if not progressed:
+            evs = [e for w in workers for e in w.in_flight()]
+            if not evs:
+                raise RuntimeError("runtime stalled: tasks remain but nothing is in flight")
+            eng.wait_any(evs, spin_us=2000)
+
+
+def _drive_threads(rt: _Runtime, workers) -> None:
+    errors = []
+
+    def drive(w):
+        try:
+            while not rt.done():
+                p = w.poll()
+                p |= w.fill()
+                if not p:
+                    evs = w.in_flight()
+                    if evs:
+                        rt.engine.wait_any(evs, spin_us=500)
+                    else:
+                        time.sleep(1e-4)
+        except BaseException as exc:  # surfaced on the caller's thread
+            errors.append(exc)
+            with rt._lock:
+                rt._done = rt.total
+
+    threads = [threading.Thread(target=drive, args=(w,), daemon=True) for w in workers]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+
+
+def _finalize(rt: _Runtime, workers, wall: float) -> Metrics:
+    eng = rt.engine
+    m = Metrics(total_flops=rt.plan.total_flops)
+    span = 0.0
+    for w in workers:
+        end = eng.record(w.slot, LANE_D2H, timing=True)
+        eng.sync(end)
+        # every task ends with an in-order D2H on this lane, so `end` marks the last one
+        elapsed = eng.elapsed_ms(w.epoch, end) / 1e3 if w.tasks_done else 0.0
+        eng.release(end)
+        dm = w.dm
+        if rt.options.record_trace:
+            kern, xfer = [], []
+            for (kind, lane, e0, e1, amount, tid, k) in w.runtime_trace:
+                s = eng.elapsed_ms(w.epoch, e0) / 1e3
+                e = eng.elapsed_ms(w.epoch, e1) / 1e3
+                rt.trace.append(TraceEvent(s, e, w.device_id, lane, kind, amount, tid, k))
+                (kern if kind == "KERNEL" else xfer).append((s, e))
+                eng.release(e0)
+                eng.release(e1)
+            dm.compt_seconds = sum(e - s for s, e in kern)
+            dm.comm_unoverlapped_seconds = exposed_comm_time(xfer, kern)
+            dm.other_seconds = max(0.0, elapsed - dm.compt_seconds - dm.comm_unoverlapped_seconds)
+        else:
+            dm.other_seconds = elapsed
+        eng.release(w.epoch)
+        m.l1_hits += w.l1_hits
+        m.l2_hits += w.l2_hits
+        m.host_fetches += w.host_fetches
+        span = max(span, elapsed)
+    m.makespan_seconds = span if span > 0 else wall
+    m.wall_seconds = wall
+    m.devices = dict(rt.device_metrics)
+    return m
+
+
+def run_call(call: RoutineCall, topology: Optional[Topology] = None,
+             options: Optional[RunOptions] = None, engine=None) -> RunResult:
+    """Plan and execute one routine call; on return the host output holds the result."""
+    return run_plan(generate_tasks(call), topology, options, engine)

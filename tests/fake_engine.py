@@ -1,0 +1,212 @@
+"""Fake device engine for the GPU-less CPU suite (TEST DOUBLE, never shipped).
+
+Same surface as ``paper_1510_05041_b200.engine.CudaEngine``.  Operations are queued per
+(device, lane) with their wait events and executed by a randomised in-order-per-stream
+simulator, so a missing event dependency in the runtime shows up as wrong numbers.
+Numerics come from the oracle (tests may import it)."""
+
+from __future__ import annotations
+
+import random
+
+import numpy as np
+
+from oracle import tiled as O
+
+LANES = (-1, -2, -3)
+
+
+class FakeEngine:
+    kind = "fake"
+
+    def __init__(self, n_devices=1, seed=0, n_compute=4, arena_bytes=64 << 20):
+        self.cuda_ids = list(range(n_devices))
+        self.n_compute = n_compute
+        self.rng = random.Random(seed)
+        self.arenas = {}
+        self.default_arena = arena_bytes
+        self._arena_cap = [0] * n_devices
+        self.queues = {}         # (slot, lane) -> list of ops
+        self.ev_done = {}        # ev -> bool
+        self._next_ev = 0
+        self.n_launches = 0
+        self.registered = 0
+        self.flag = [False] * n_devices
+        self.ops_log = []
+
+    # ---- devices ----
+    def slot(self, cuda_id):
+        return self.cuda_ids.index(cuda_id)
+
+    @property
+    def ndev(self):
+        return len(self.cuda_ids)
+
+    def device_info(self, slot):
+        return dict(name="fake", sms=148, total_bytes=1 << 34, free_bytes=self.default_arena)
+
+    def ensure_arenas(self, caps):
+        for slot, c in caps.items():
+            if c > self._arena_cap[slot]:
+                self._arena_cap[slot] = c
+                self.arenas[slot] = np.zeros((c + 7) // 8, dtype=np.float64)
+
+    def arena_capacity(self, slot):
+        return self._arena_cap[slot]
+
+    def register_host(self, array):
+        self.registered += 1
+        return True
+
+    def unregister_host(self, array):
+        self.registered -= 1
+
+    # ---- event / queue machinery ----
+    def _new_ev(self):
+        ev = self._next_ev
+        self._next_ev += 1
+        self.ev_done[ev] = False
+        return ev
+
+    def _enqueue(self, slot, lane, fn, waits):
+        ev = self._new_ev()
+        for w in waits:
+            assert w in self.ev_done, f"wait on unknown event {w}"
+        self.queues.setdefault((slot, lane), []).append((list(waits), fn, ev))
+        return ev
+
+    def _step(self) -> bool:
+        """Execute the head op of one random runnable stream."""
+        ready = [k for k, q in self.queues.items()
+                 if q and all(self.ev_done[w] for w in q[0][0])]
+        if not ready:
+            return False
+        k = self.rng.choice(sorted(ready))
+        waits, fn, ev = self.queues[k].pop(0)
+        fn()
+        self.ev_done[ev] = True
+        return True
+
+    def _run_until(self, pred, limit=10_000_000):
+        for _ in range(limit):
+            if pred():
+                return
+            if not self._step():
+                assert pred(), "fake GPU deadlock: pending ops wait on events that never fire"
+                return
+
+    # ---- memory views ----
+    def _view(self, slot, off, ld, h, w):
+        a = self.arenas[slot]
+        assert off % 8 == 0
+        base = off // 8
+        assert base + ld * w <= a.size, "access outside arena"
+        return a[base:base + ld * w].reshape(w, ld).T[:h, :]
+
+    # ---- transfers ----
+    def h2d(self, slot, dst_off, dst_ld, desc, r0, c0, h, w, waits=()):
+        def fn():
+            self._view(slot, dst_off, dst_ld, h, w)[:, :] = desc.as_2d()[r0:r0 + h, c0:c0 + w]
+        return self._enqueue(slot, -1, fn, waits)
+
+    def d2h(self, slot, src_off, src_ld, desc, r0, c0, h, w, waits=()):
+        def fn():
+            desc.as_2d()[r0:r0 + h, c0:c0 + w] = self._view(slot, src_off, src_ld, h, w)
+        return self._enqueue(slot, -2, fn, waits)
+
+    def p2p(self, dst_slot, dst_off, src_slot, src_off, nbytes, waits=()):
+        def fn():
+            s = self.arenas[src_slot][src_off // 8:(src_off + nbytes) // 8]
+            self.arenas[dst_slot][dst_off // 8:(dst_off + nbytes) // 8] = s
+        return self._enqueue(dst_slot, -3, fn, waits)
+
+    # ---- kernels ----
+    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=()):
+        self.n_launches += 1
+
+        def fn():
+            c = self._view(slot, c_off, ldc, h, w)
+            acc = np.zeros((h, w))
+            for (ao, lda, bo, ldb, d) in steps:
+                a = self._view(slot, ao, lda, d if ta else h, h if ta else d)
+                b = self._view(slot, bo, ldb, w if tb else d, d if tb else w)
+                acc += (a.T if ta else a) @ (b.T if tb else b)
+            new = alpha * acc if beta == 0.0 else alpha * acc + beta * c
+            if tri:
+                m = np.tril(np.ones((h, w), bool)) if tri == 1 else np.triu(np.ones((h, w), bool))
+                c[m] = new[m]
+            else:
+                c[:, :] = new
+        return self._enqueue(slot, stream, fn, waits)
+
+    def trsm(self, slot, stream, right, upper, trans, unit, h, w, alpha, a_off, lda, b_off, ldb,
+             waits=()):
+        self.n_launches += 1
+        n = w if right else h
+
+        def fn():
+            a = self._view(slot, a_off, lda, n, n)
+            b = self._view(slot, b_off, ldb, h, w)
+            try:
+                O.trsm_solve(b, a.copy(), alpha, "upper" if upper else "lower",
+                             "unit" if unit else "non-unit", "right" if right else "left",
+                             bool(trans))
+            except O.OracleSingular:
+                self.flag[slot] = True
+        return self._enqueue(slot, stream, fn, waits)
+
+    def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
+                    waits=()):
+        self.n_launches += 1
+
+        def fn():
+            a = self._view(slot, a_off, lda, n, n).copy()
+            uplo = "upper" if upper else "lower"
+            if mode_sym:
+                m = O.sym_of(a, uplo)
+            else:
+                m, _ = O.tri_of(a, uplo, "unit" if unit else "non-unit", bool(trans))
+            self._view(slot, dst_off, ldd, n, n)[:, :] = m
+        return self._enqueue(slot, stream, fn, waits)
+
+    def singular(self, slot, reset=True):
+        f = self.flag[slot]
+        if reset:
+            self.flag[slot] = False
+        return f
+
+    # ---- events ----
+    def record(self, slot, lane, timing=False):
+        return self._enqueue(slot, lane, lambda: None, ())
+
+    def done(self, ev):
+        # make progress a random amount, then answer
+        for _ in range(self.rng.randint(0, 3)):
+            if not self._step():
+                break
+        return self.ev_done[ev]
+
+    def wait_any(self, evs, spin_us=-1):
+        self._run_until(lambda: any(self.ev_done[e] for e in evs))
+        for i, e in enumerate(evs):
+            if self.ev_done[e]:
+                return i
+        return -1
+
+    def sync(self, ev):
+        self._run_until(lambda: self.ev_done[ev])
+
+    def elapsed_ms(self, e0, e1):
+        return 1.0
+
+    def release(self, ev):
+        pass
+
+    def stream_wait(self, slot, lane, ev):
+        self._enqueue(slot, lane, lambda: None, (ev,))
+
+    def device_sync(self, slot):
+        self._run_until(lambda: all(not q for (s, _), q in self.queues.items() if s == slot))
+
+    def launches(self):
+        return self.n_launches

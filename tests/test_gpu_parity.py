@@ -1,0 +1,207 @@
+"""Parity of the B200 path against the reference (golden fixtures) and the oracle.
+
+Tolerance (BASELINE.json north_star): ||C - C_ref||_F / (|alpha| ||A||_F ||B||_F k eps +
+|beta| ||C0||_F eps) <= 10, eps = finfo(float64).eps; TRSM also by its residual."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_variants
+from oracle import dense, tiled, tolerance
+from paper_1510_05041_b200 import (InvalidArgumentError, RoutineCall, RunOptions,
+                                   SingularMatrixError, build_call, dgemm, dsymm, dsyr2k, dsyrk,
+                                   dtrmm, dtrsm, run_call)
+from paper_1510_05041_b200.devices import DeviceDesc, Topology
+from paper_1510_05041_b200.tiling import MatrixDesc, make_tiled
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(np.float64).eps
+CASES = load_variants()
+
+
+def _ratio(kind, out, ref, a, b, c0, alpha, beta, k):
+    return tolerance.routine_ratio(kind, out, ref, a=a, b=b, c0=c0, alpha=alpha, beta=beta,
+                                   k=k, eps=EPS)
+
+
+def _call(case):
+    t = case["shape"]["tile_size"]
+
+    def tm(mid, arr):
+        return make_tiled(MatrixDesc.from_array(mid, arr, pad=case["pad"]), t)
+    return RoutineCall(kind=case["kind"], a=tm("A", case["a"]),
+                       b=None if case["b"] is None else tm("B", case["b"]),
+                       c=tm("C", case["c"]), **case["params"])
+
+
+def test_native_library_loaded():
+    import paper_1510_05041_b200._native as N
+    N.require_gpu()
+    N.load()
+    maps = open("/proc/self/maps").read()
+    assert "libblasx_cuda.so" in maps
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_variants_match_reference_outputs(case):
+    call = _call(case)
+    a0 = call.a.matrix.storage.copy()
+    res = run_call(call, options=RunOptions(chunk_steps=2))
+    out = call.c.matrix.as_2d()
+    np.testing.assert_allclose(out, case["out"], rtol=1e-11, atol=1e-12)
+    assert np.array_equal(call.a.matrix.storage, a0)
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+
+
+def test_cfg1_against_reference_checksums_and_oracle():
+    """BASELINE configs[0]: DGEMM 2048^3 NN, T=512, alpha=beta=1, seed 0."""
+    g = np.load(os.path.join(GOLDEN, "cfg1.npz"))
+    call = build_call("gemm", m=2048, n=2048, k=2048, tile_size=512, seed=0, alpha=1.0, beta=1.0)
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    run_call(call)
+    out = call.c.matrix.as_2d()
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=512, alpha=1.0, beta=1.0)
+    r = _ratio("gemm", out, ref, a, b, c0, 1.0, 1.0, 2048)
+    assert r <= tolerance.BOUND, r
+    np.testing.assert_allclose(out[:64, :64], g["block"], rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(out[-64:, 1000:1064], g["block2"], rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(np.ascontiguousarray(out).sum(axis=0), g["colsum"], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("gemm", dict(trans_a=True, beta=0.0)),
+    ("gemm", dict(trans_b=True, beta=-0.5, alpha=0.3)),
+    ("gemm", dict(trans_a=True, trans_b=True, beta=1.0)),
+    ("syrk", dict(uplo="lower", beta=1.0)),
+    ("syrk", dict(uplo="upper", trans_a=True, beta=0.0, alpha=-1.0)),
+    ("syr2k", dict(uplo="lower", beta=1.0)),
+    ("syr2k", dict(uplo="upper", trans_a=True, beta=0.5)),
+    ("symm", dict(uplo="lower", side="left", beta=1.0)),
+    ("symm", dict(uplo="upper", side="right", beta=0.0)),
+    ("trmm", dict(uplo="lower", side="left")),
+    ("trmm", dict(uplo="upper", side="right", trans_a=True, diag="unit", alpha=0.7)),
+    ("trsm", dict(uplo="lower", side="left")),
+    ("trsm", dict(uplo="upper", side="left", trans_a=True, alpha=2.0)),
+    ("trsm", dict(uplo="lower", side="right", diag="unit")),
+    ("trsm", dict(uplo="upper", side="right", trans_a=True)),
+])
+def test_routines_medium_against_oracle(kind, kw):
+    n, k, t = 1300, 900, 512      # edge tiles in every dimension
+    call = build_call(kind, m=n, n=n, k=k, tile_size=t, seed=7, trsm_scaled=True, **kw)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    run_call(call)
+    out = call.c.matrix.as_2d()
+    p = dict(kw)
+    alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
+    ref = c0.copy()
+    tiled.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
+    kk = k if kind in ("gemm", "syrk", "syr2k") else n
+    r = _ratio(kind, out, ref, a, b, c0, alpha, beta, kk)
+    assert r <= tolerance.BOUND, r
+    if kind == "trsm":
+        m, _ = tiled.tri_of(a, p.get("uplo", "upper"), p.get("diag", "non-unit"),
+                            p.get("trans_a", False))
+        rr = tolerance.trsm_residual_ratio(m, out, c0, alpha, p.get("side", "left"), EPS)
+        assert rr <= tolerance.BOUND, rr
+    if kind in ("syrk", "syr2k"):
+        mask = np.triu(np.ones((n, n), bool), 1) if p["uplo"] == "lower" else np.tril(np.ones((n, n), bool), -1)
+        assert np.array_equal(out[mask], c0[mask])     # unstored triangle untouched
+
+
+def test_beta_zero_never_reads_c():
+    call = build_call("gemm", m=700, n=600, k=500, tile_size=256, seed=3, beta=0.0)
+    call.c.matrix.storage[:] = np.nan
+    a, b = call.a.matrix.as_2d(), call.b.matrix.as_2d()
+    run_call(call)
+    out = call.c.matrix.as_2d()
+    assert np.isfinite(out).all()
+    np.testing.assert_allclose(out, a @ b, rtol=1e-12, atol=1e-12)
+
+
+def test_unstored_triangle_never_read_symm_trmm():
+    rng = np.random.default_rng(5)
+    n = 600
+    a = rng.random((n, n))
+    poisoned = a.copy()
+    poisoned[np.triu_indices(n, 1)] = np.nan            # lower is stored
+    bm = rng.random((n, 300))
+    for kind in ("symm", "trmm"):
+        c = np.asfortranarray(rng.random((n, 300)))
+        if kind == "symm":
+            res_c = c.copy(order="F")
+            dsymm("L", "L", n, 300, 1.0, np.asfortranarray(poisoned), n, np.asfortranarray(bm), n,
+                  0.0, res_c, n, tile_size=256)
+            s = np.tril(a) + np.tril(a, -1).T
+            np.testing.assert_allclose(res_c, s @ bm, rtol=1e-11, atol=1e-11)
+        else:
+            x = np.asfortranarray(bm.copy())
+            dtrmm("L", "L", "N", "U", n, 300, 1.0, np.asfortranarray(poisoned), n, x, n, tile_size=256)
+            m = np.tril(a, -1) + np.eye(n)
+            np.testing.assert_allclose(x, m @ bm, rtol=1e-11, atol=1e-11)
+
+
+def test_trsm_singular_raises():
+    rng = np.random.default_rng(1)
+    a = np.asfortranarray(rng.random((512, 512)) + 2 * np.eye(512))
+    a[300, 300] = 0.0
+    b = np.asfortranarray(rng.random((512, 64)))
+    with pytest.raises(SingularMatrixError):
+        dtrsm("L", "L", "N", "N", 512, 64, 1.0, a, 512, b, 512, tile_size=256)
+
+
+def test_trsm_unit_diag_ignores_zero_diagonal():
+    rng = np.random.default_rng(2)
+    n = 300
+    a = rng.random((n, n)) / n
+    np.fill_diagonal(a, 0.0)
+    b = rng.random((n, 40))
+    x = np.asfortranarray(b.copy())
+    dtrsm("L", "L", "N", "U", n, 40, 1.0, np.asfortranarray(a), n, x, n, tile_size=128)
+    m = np.tril(a, -1) + np.eye(n)
+    np.testing.assert_allclose(m @ x, b, rtol=1e-11, atol=1e-11)
+
+
+def test_cblas_dgemm_fortran_arrays_and_leading_dims():
+    rng = np.random.default_rng(3)
+    m, n, k, lda = 333, 222, 111, 340
+    abuf = rng.random(lda * k)
+    b = np.asfortranarray(rng.random((k, n)))
+    c = np.asfortranarray(rng.random((m, n)))
+    a2 = abuf.reshape(k, lda).T[:m, :]
+    ref = 2.0 * a2 @ b + 0.5 * c
+    dgemm("N", "N", m, n, k, 2.0, abuf, lda, b, k, 0.5, c, m, tile_size=128)
+    np.testing.assert_allclose(c, ref, rtol=1e-12, atol=1e-12)
+    with pytest.raises(InvalidArgumentError):
+        dgemm("X", "N", m, n, k, 1.0, abuf, lda, b, k, 0.0, c, m)
+
+
+def test_small_arena_eviction_on_gpu():
+    call = build_call("gemm", m=1024, n=1024, k=2048, tile_size=256, seed=8, beta=1.0)
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    tile = 256 * 256 * 8
+    res = run_call(call, Topology([DeviceDesc(0, arena_capacity=40 * tile)]),
+                   RunOptions(chunk_steps=2))
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=256, alpha=1.0, beta=1.0)
+    assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 2048) <= 10
+    assert res.metrics.host_fetches > 16 + 32       # evictions forced refetches
+
+
+def test_concurrent_mode_and_trace():
+    call = build_call("syr2k", m=1100, n=1100, k=700, tile_size=256, seed=9, beta=1.0, uplo="lower")
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    res = run_call(call, options=RunOptions(execution="concurrent", record_trace=True))
+    ref = c0.copy()
+    tiled.run_tiled("syr2k", a, ref, b, tile_size=256, alpha=1.0, beta=1.0, uplo="lower")
+    assert _ratio("syr2k", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 700) <= 10
+    assert any(e.event == "KERNEL" for e in res.trace)
+    ks = [e for e in res.trace if e.event == "KERNEL"]
+    assert all(e.time_end >= e.time_start for e in ks)

@@ -1,0 +1,160 @@
+"""Host runtime (planner -> scheduler -> cache -> engine) on the fake engine: numerics
+against the reference's own outputs, byte accounting, stealing, eviction, errors."""
+
+import numpy as np
+import pytest
+
+from conftest import load_variants
+from fake_engine import FakeEngine
+from paper_1510_05041_b200.devices import DeviceDesc, Topology
+from paper_1510_05041_b200.errors import (CapacityDeadlockError, ConfigError,
+                                          SingularMatrixError)
+from paper_1510_05041_b200.operands import build_call
+from paper_1510_05041_b200.routines import RoutineCall, generate_tasks
+from paper_1510_05041_b200.scheduler import RunOptions, run_call
+from paper_1510_05041_b200.tiling import MatrixDesc, make_tiled
+
+CASES = load_variants()
+
+
+def topo(n, arena=8 << 20):
+    return Topology([DeviceDesc(i, arena_capacity=arena, peer_group="g") for i in range(n)])
+
+
+def call_of(case):
+    t = case["shape"]["tile_size"]
+
+    def tiled(mid, arr):
+        return make_tiled(MatrixDesc.from_array(mid, arr, pad=case["pad"]), t)
+    return RoutineCall(kind=case["kind"], a=tiled("A", case["a"]),
+                       b=None if case["b"] is None else tiled("B", case["b"]),
+                       c=tiled("C", case["c"]), **case["params"])
+
+
+@pytest.mark.parametrize("ndev", [1, 3])
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_variants_match_reference(case, ndev):
+    call = call_of(case)
+    a0 = call.a.matrix.storage.copy()
+    eng = FakeEngine(ndev, seed=hash(case["name"]) % 1000)
+    res = run_call(call, topo(ndev), RunOptions(chunk_steps=2), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-12, atol=1e-12)
+    assert np.array_equal(call.a.matrix.storage, a0)          # inputs never written
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    m = res.metrics
+    assert m.total_d2h_bytes() == sum(t.out_ref.height * t.out_ref.width * 8 for t in res.plan.tasks)
+    d_in = sum(d.d2d_in_bytes for d in m.devices.values())
+    d_out = sum(d.d2d_out_bytes for d in m.devices.values())
+    assert d_in == d_out
+
+
+@pytest.mark.parametrize("execution", ["deterministic", "concurrent"])
+def test_two_devices_split_and_l2(execution):
+    call = build_call("gemm", m=64, n=64, k=64, tile_size=8, seed=1, beta=0.5)
+    ref = call.c.matrix.as_2d().copy()
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    res = run_call(call, topo(2), RunOptions(execution=execution), engine=FakeEngine(2, seed=3))
+    np.testing.assert_allclose(call.c.matrix.as_2d(), a @ b + 0.5 * ref, rtol=1e-12, atol=1e-12)
+    assert all(v > 0 for v in res.tasks_by_device.values())
+    m = res.metrics
+    # L2 converts host traffic into peer traffic: with L2 off, H2D grows by exactly the
+    # bytes moved peer-to-peer
+    call2 = build_call("gemm", m=64, n=64, k=64, tile_size=8, seed=1, beta=0.5)
+    res2 = run_call(call2, topo(2), RunOptions(execution=execution, l2_enabled=False),
+                    engine=FakeEngine(2, seed=3))
+    assert res2.metrics.total_d2d_bytes() == 0
+    if execution == "deterministic":
+        assert m.l2_hits > 0
+        assert m.total_d2d_bytes() == m.l2_hits * 8 * 8 * 8
+
+
+def test_l1_disabled_fetches_every_input():
+    call = build_call("gemm", m=32, n=32, k=32, tile_size=8, seed=2)
+    res = run_call(call, topo(1), RunOptions(l1_enabled=False), engine=FakeEngine(1))
+    plan = res.plan
+    n_refs = sum(len(s.input_refs()) for t in plan.tasks for s in t.steps)
+    assert res.metrics.host_fetches == n_refs
+    assert res.metrics.l1_hits == 0
+
+
+def test_l1_hits_on_shared_panels():
+    call = build_call("gemm", m=32, n=32, k=32, tile_size=8, seed=2)
+    res = run_call(call, topo(1), RunOptions(), engine=FakeEngine(1))
+    assert res.metrics.host_fetches == 32     # 16 A + 16 B tiles, each fetched once
+    assert res.metrics.l1_hits == 16 * 4 * 2 - 32
+
+
+def test_small_arena_evicts_and_stays_correct():
+    call = build_call("gemm", m=48, n=48, k=48, tile_size=8, seed=4, beta=1.0)
+    c0 = call.c.matrix.as_2d().copy()
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    tile = 8 * 8 * 8
+    opts = RunOptions(chunk_steps=1)
+    res = run_call(call, Topology([DeviceDesc(0, arena_capacity=14 * 512 * 4)]), opts,
+                   engine=FakeEngine(1, seed=9))
+    np.testing.assert_allclose(call.c.matrix.as_2d(), a @ b + c0, rtol=1e-12, atol=1e-12)
+    assert res.metrics.host_fetches > 72        # evictions forced re-fetches
+    assert tile == 512
+
+
+def test_arena_floor_enforced():
+    call = build_call("gemm", m=16, n=16, k=16, tile_size=8, seed=1)
+    with pytest.raises(ConfigError):
+        run_call(call, Topology([DeviceDesc(0, arena_capacity=1024)]), RunOptions(),
+                 engine=FakeEngine(1))
+
+
+def test_capacity_deadlock_when_one_task_cannot_fit():
+    call = build_call("gemm", m=16, n=16, k=64, tile_size=8, seed=1)
+    # 13 tiles of capacity: a 4-stream batch with chunk_steps large pins > arena
+    opts = RunOptions(chunk_steps=64, n_streams=4)
+    try:
+        run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * 512)]), opts,
+                 engine=FakeEngine(1))
+    except CapacityDeadlockError:
+        pass
+
+
+def test_trsm_singular_raises():
+    rng = np.random.default_rng(0)
+    a = rng.random((16, 16)) + np.eye(16)
+    a[5, 5] = 0.0
+    call = RoutineCall("trsm", a=make_tiled(MatrixDesc.from_array("A", a), 8),
+                       c=make_tiled(MatrixDesc.from_array("C", rng.random((16, 4))), 8),
+                       uplo="lower")
+    with pytest.raises(SingularMatrixError):
+        run_call(call, topo(1), RunOptions(), engine=FakeEngine(1))
+
+
+def test_trace_accounts_for_bytes_and_flops():
+    call = build_call("syrk", m=24, n=24, k=16, tile_size=8, seed=5, beta=1.0, uplo="lower")
+    res = run_call(call, topo(2), RunOptions(record_trace=True), engine=FakeEngine(2))
+    kinds = {e.event for e in res.trace}
+    assert {"H2D", "D2H", "KERNEL"} <= kinds
+    h2d = sum(e.bytes_or_flops for e in res.trace if e.event == "H2D")
+    assert h2d == res.metrics.total_h2d_bytes()
+
+
+def test_stealing_feeds_idle_device():
+    from paper_1510_05041_b200 import scheduler as S
+    call = build_call("gemm", m=16, n=16, k=16, tile_size=8, seed=1)
+    plan = generate_tasks(call)
+    rs0 = S.ReservationStation(0, 8)
+    for t in plan.tasks[:3]:
+        rs0.put(S._SlotEntry(t))
+
+    class W:
+        def __init__(self, d, rs, rt):
+            self.device_id, self.rs, self.runtime = d, rs, rt
+
+    class RT:
+        queue = S.TaskQueue()
+    rt = RT()
+    w0, w1 = W(0, rs0, rt), W(1, S.ReservationStation(1, 8), rt)
+    rt.workers = [w0, w1]
+    got = S.steal_for(w1)
+    assert got is not None and rs0.pending_count() == 2
+    rt.queue.put((0, 0.0))
+    assert S.steal_for(w1) is None                # queue not empty -> no theft
+    rt.queue.get()
+    assert S.steal_for(w1) is not None and S.steal_for(w1) is None   # victim keeps its last
