@@ -66,6 +66,7 @@ _SIGS = {
     "bx_dev_copy_d2h": [_i, _p, _u64, _u64],
     "bx_dgemm_device": [_i, _i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _d, _u64, _i],
     "bx_fp64_peak_probe": [_i, _i, C.POINTER(C.c_double)],
+    "bx_set_gemm_variant": [_i],
     "bx_last_error": [C.c_char_p, _i],
 }
 

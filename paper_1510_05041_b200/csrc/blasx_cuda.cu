@@ -145,17 +145,43 @@ bool need_attr(unsigned bit) {
   return true;
 }
 
-template <bool TA, bool TB>
-int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
-  if (need_attr(1u << ((TA ? 2 : 0) + (TB ? 1 : 0)))) {
-    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  bx::G_SMEM_BYTES));
+int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
+
+template <class Cfg, bool TA, bool TB>
+int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
+  if (need_attr(bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM_BYTES));
   }
-  int tiles = ((t.h + bx::G_BM - 1) / bx::G_BM) * ((t.w + bx::G_BN - 1) / bx::G_BN);
-  bx::gemm_task_kernel<TA, TB><<<tiles, bx::G_THREADS, bx::G_SMEM_BYTES, s>>>(t);
+  int tiles = ((t.h + Cfg::BM - 1) / Cfg::BM) * ((t.w + Cfg::BN - 1) / Cfg::BN);
+  bx::gemm_task_kernel<Cfg, TA, TB><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(t);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return BX_OK;
+}
+
+template <class Cfg, bool TA, bool TB>
+int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
+  if (need_attr(bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_mb_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM_BYTES));
+  }
+  int tiles = ((t.h + Cfg::BM - 1) / Cfg::BM) * ((t.w + Cfg::BN - 1) / Cfg::BN);
+  bx::gemm_task_mb_kernel<Cfg, TA, TB><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(t);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+template <bool TA, bool TB>
+int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
+  unsigned tb = (TA ? 2u : 0u) + (TB ? 1u : 0u);
+  switch (g_gemm_variant) {
+    case 1: return launch_gemm_cfg<bx::CfgWide, TA, TB>(t, s, 1u << (16 + tb));
+    case 2: return launch_gemm_cfg<bx::CfgDeep, TA, TB>(t, s, 1u << (24 + tb));
+    case 3: return launch_gemm_ws<bx::CfgMb2, TA, TB>(t, s, 1u << (20 + tb));
+    default: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s, 1u << (12 + tb));
+  }
 }
 
 int launch_gemm(int ta, int tb, const bx::GemmTask& t, cudaStream_t s) {
@@ -723,6 +749,11 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
   const double* ap = (const double*)a;
   const double* bp = (const double*)b;
   return gemm_raw(s, ta, tb, 0, m, n, 1, &ap, &lda, &bp, &ldb, &k, alpha, beta, (double*)c, ldc);
+}
+
+int bx_set_gemm_variant(int v) {
+  g_gemm_variant = v;
+  return BX_OK;
 }
 
 int bx_fp64_peak_probe(int dev, int iters, double* tflops) {

@@ -13,21 +13,16 @@
 //
 // Device tile layout (chosen by the transfer engine): column-major,
 // leading dimension a multiple of 8 elements, base 256-B aligned.  Operands are staged
-// into shared memory with 16-B cp.async (zero-filled past the tile edge), in one of two
-// layouts per operand so both layouts are bank-conflict free for the DMMA fragment
-// loads:  "MN-major" sX[k][mn] (row pitch 132) when mn is the contiguous direction
-// in global memory, "K-major" sX[mn][k] (row pitch 20) when k is.
+// into shared memory with 16-B cp.async (zero-filled past the tile edge) in one of two
+// layouts per operand, both bank-conflict free for the DMMA fragment loads (pitch = 4
+// mod 16 doubles): "MN-major" sX[k][mn] when mn is the contiguous direction in global
+// memory, "K-major" sX[mn][k] when k is.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace bx {
 
-constexpr int G_BM = 128, G_BN = 128, G_BK = 16, G_STAGES = 4, G_THREADS = 256;
-constexpr int G_LD_MN = G_BM + 4;   // 132 doubles: conflict-free frag loads (132 = 4 mod 16)
-constexpr int G_LD_K = G_BK + 4;    // 20 doubles
-constexpr int G_STAGE_ELEMS = (G_BK * G_LD_MN > G_BM * G_LD_K) ? G_BK * G_LD_MN : G_BM * G_LD_K;
-constexpr int G_SMEM_BYTES = G_STAGES * 2 * G_STAGE_ELEMS * 8;
 constexpr int G_MAX_STEPS = 40;
 
 enum TriMode { TRI_NONE = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
@@ -45,6 +40,24 @@ struct GemmTask {
   GemmStep steps[G_MAX_STEPS];
 };
 
+// Tile configuration: CTA BM x BN x BK, warp tile WM x WN, STAGES-deep cp.async ring.
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int MF = WM / 8, NF = WN / 8;
+  static constexpr int LD_K = BK + 4;  // K-major pitch (doubles), = 4 mod 16
+  static constexpr int A_ELEMS = (BK * (BM + 4) > BM * LD_K) ? BK * (BM + 4) : BM * LD_K;
+  static constexpr int B_ELEMS = (BK * (BN + 4) > BN * LD_K) ? BK * (BN + 4) : BN * LD_K;
+  static constexpr int SMEM_BYTES = STAGES * (A_ELEMS + B_ELEMS) * 8;
+  static_assert((BM + 4) % 16 == 4 && (BN + 4) % 16 == 4 && LD_K % 16 == 4, "pitch");
+  static_assert((BM * BK / 2) % THREADS == 0 && (BN * BK / 2) % THREADS == 0, "load split");
+};
+
+using CfgWide = GemmCfg<128, 128, 16, 64, 32, 4>;     // 8 warps, 2 warps/SMSP
+using CfgDeep = GemmCfg<128, 128, 32, 32, 32, 3>;     // 16 warps, 4 warps/SMSP
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
@@ -58,119 +71,118 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-// Stage one BK-deep slab of op(A) rows [m0, m0+128) (TA: A stored transposed) or
-// op(B) cols [n0, n0+128) into shared memory.  `mn_ext` is the tile extent along mn
-// (h for A, w for B), `d` the step depth, `k0` the slab start within the step.
+// Stage one BK-deep slab of op(X) along mn in [mn0, mn0+EXT) into shared memory.
 // KCONTIG: k is the contiguous direction in global memory -> K-major smem.
-template <bool KCONTIG>
+template <class Cfg, int EXT, bool KCONTIG>
 __device__ __forceinline__ void load_slab(double* s, const double* g, int ld, int mn0, int mn_ext,
                                           int k0, int d, int tid) {
+  constexpr int BK = Cfg::BK;
+  constexpr int KCH = BK / 2;      // 16-B chunks per mn row (K-major)
+  constexpr int MCH = EXT / 2;     // 16-B chunks per k row (MN-major)
 #pragma unroll
-  for (int c = 0; c < (G_BM * G_BK / 2) / G_THREADS; ++c) {
-    int idx = tid + c * G_THREADS;
+  for (int c = 0; c < (EXT * BK / 2) / Cfg::THREADS; ++c) {
+    int idx = tid + c * Cfg::THREADS;
     if (KCONTIG) {
-      int mn = idx >> 3, k = (idx & 7) * 2;
+      int mn = idx / KCH, k = (idx % KCH) * 2;
       int gm = mn0 + mn, gk = k0 + k;
       int valid = (gm < mn_ext) ? min(max(d - gk, 0), 2) : 0;
       const double* src = valid ? g + (size_t)gm * ld + gk : g;
-      cp_async16(s + mn * G_LD_K + k, src, valid * 8);
+      cp_async16(s + mn * Cfg::LD_K + k, src, valid * 8);
     } else {
-      int k = idx >> 6, mn = (idx & 63) * 2;
+      int k = idx / MCH, mn = (idx % MCH) * 2;
       int gm = mn0 + mn, gk = k0 + k;
       int valid = (gk < d) ? min(max(mn_ext - gm, 0), 2) : 0;
       const double* src = valid ? g + (size_t)gk * ld + gm : g;
-      cp_async16(s + k * G_LD_MN + mn, src, valid * 8);
+      cp_async16(s + k * (EXT + 4) + mn, src, valid * 8);
     }
   }
 }
 
-template <bool KMAJ>
+template <class Cfg, int EXT, bool KMAJ>
 __device__ __forceinline__ double frag(const double* s, int mn, int k) {
-  return KMAJ ? s[mn * G_LD_K + k] : s[k * G_LD_MN + mn];
+  return KMAJ ? s[mn * Cfg::LD_K + k] : s[k * (EXT + 4) + mn];
 }
 
-// TA/TB: operand stored transposed (op = T).  A is MN-contiguous iff !TA; B is
-// K-contiguous iff !TB.
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(G_THREADS, 1) gemm_task_kernel(const __grid_constant__ GemmTask t) {
+// TA/TB: operand stored transposed (op = T).  A is K-contiguous iff TA; B iff !TB.
+template <class Cfg, bool TA, bool TB>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_kernel(const __grid_constant__ GemmTask t) {
   extern __shared__ __align__(128) double smem[];
-  constexpr bool A_KMAJ = TA;    // A: (m,k) at a[k + m*lda] when TA -> k contiguous
-  constexpr bool B_KMAJ = !TB;   // B: (k,n) at b[k + n*ldb] when !TB -> k contiguous
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int MF = Cfg::MF, NF = Cfg::NF;
+  constexpr bool A_KMAJ = TA;
+  constexpr bool B_KMAJ = !TB;
 
   // grouped rasterisation of a 1-D grid (L2 reuse when one launch spans many tiles)
-  const int tiles_m = (t.h + G_BM - 1) / G_BM, tiles_n = (t.w + G_BN - 1) / G_BN;
-  int bid = blockIdx.x;
-  int gm = t.group_m;
-  int per_group = gm * tiles_n;
-  int group = bid / per_group;
-  int first_m = group * gm;
-  int gsize = min(tiles_m - first_m, gm);
-  int bm = first_m + (bid % per_group) % gsize;
-  int bn = (bid % per_group) / gsize;
-  const int m0 = bm * G_BM, n0 = bn * G_BN;
-  if (t.tri == TRI_LOWER && n0 >= m0 + G_BM) return;   // wholly above the diagonal
-  if (t.tri == TRI_UPPER && m0 >= n0 + G_BN) return;   // wholly below
+  const int tiles_m = (t.h + BM - 1) / BM, tiles_n = (t.w + BN - 1) / BN;
+  const int bid = blockIdx.x;
+  const int per_group = t.group_m * tiles_n;
+  const int first_m = (bid / per_group) * t.group_m;
+  const int gsize = min(tiles_m - first_m, t.group_m);
+  const int bm = first_m + (bid % per_group) % gsize;
+  const int bn = (bid % per_group) / gsize;
+  const int m0 = bm * BM, n0 = bn * BN;
+  if (t.tri == TRI_LOWER && n0 >= m0 + BM) return;   // wholly above the diagonal
+  if (t.tri == TRI_UPPER && m0 >= n0 + BN) return;   // wholly below
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, q = lane & 3;
 
-  // total number of BK slabs over all steps
   int total = 0;
-  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + G_BK - 1) / G_BK;
+  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + BK - 1) / BK;
 
   double* sA = smem;
-  double* sB = smem + G_STAGES * G_STAGE_ELEMS;
+  double* sB = smem + STAGES * Cfg::A_ELEMS;
 
-  int ld_step = 0, ld_k = 0;   // producer cursor
+  int ld_step = 0, ld_k = 0;   // producer cursor over (step, k)
   auto issue = [&](int stage) {
     const GemmStep& st = t.steps[ld_step];
-    load_slab<A_KMAJ>(sA + stage * G_STAGE_ELEMS, st.a, st.lda, m0, t.h, ld_k, st.d, tid);
-    load_slab<B_KMAJ>(sB + stage * G_STAGE_ELEMS, st.b, st.ldb, n0, t.w, ld_k, st.d, tid);
-    ld_k += G_BK;
+    load_slab<Cfg, BM, A_KMAJ>(sA + stage * Cfg::A_ELEMS, st.a, st.lda, m0, t.h, ld_k, st.d, tid);
+    load_slab<Cfg, BN, B_KMAJ>(sB + stage * Cfg::B_ELEMS, st.b, st.ldb, n0, t.w, ld_k, st.d, tid);
+    ld_k += BK;
     if (ld_k >= st.d) { ld_k = 0; ++ld_step; }
   };
 
 #pragma unroll
-  for (int s = 0; s < G_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < total) issue(s);
     cp_async_commit();
   }
 
-  double acc[8][4][2];
+  double acc[MF][NF][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MF; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int it = 0; it < total; ++it) {
-    cp_async_wait<G_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      int nxt = it + G_STAGES - 1;
-      if (nxt < total) issue(nxt % G_STAGES);
+      int nxt = it + STAGES - 1;
+      if (nxt < total) issue(nxt % STAGES);
       cp_async_commit();
     }
-    const double* a = sA + (it % G_STAGES) * G_STAGE_ELEMS;
-    const double* b = sB + (it % G_STAGES) * G_STAGE_ELEMS;
-    double fa[2][8], fb[2][4];
+    const double* a = sA + (it % STAGES) * Cfg::A_ELEMS;
+    const double* b = sB + (it % STAGES) * Cfg::B_ELEMS;
+    double fa[2][MF], fb[2][NF];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) fa[0][i] = frag<A_KMAJ>(a, wm + i * 8 + g, q);
+    for (int i = 0; i < MF; ++i) fa[0][i] = frag<Cfg, BM, A_KMAJ>(a, wm + i * 8 + g, q);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) fb[0][j] = frag<B_KMAJ>(b, wn + j * 8 + g, q);
+    for (int j = 0; j < NF; ++j) fb[0][j] = frag<Cfg, BN, B_KMAJ>(b, wn + j * 8 + g, q);
 #pragma unroll
-    for (int kq = 0; kq < G_BK / 4; ++kq) {
+    for (int kq = 0; kq < BK / 4; ++kq) {
       const int cur = kq & 1, nx = cur ^ 1;
-      if (kq + 1 < G_BK / 4) {
+      if (kq + 1 < BK / 4) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) fa[nx][i] = frag<A_KMAJ>(a, wm + i * 8 + g, (kq + 1) * 4 + q);
+        for (int i = 0; i < MF; ++i) fa[nx][i] = frag<Cfg, BM, A_KMAJ>(a, wm + i * 8 + g, (kq + 1) * 4 + q);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fb[nx][j] = frag<B_KMAJ>(b, wn + j * 8 + g, (kq + 1) * 4 + q);
+        for (int j = 0; j < NF; ++j) fb[nx][j] = frag<Cfg, BN, B_KMAJ>(b, wn + j * 8 + g, (kq + 1) * 4 + q);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MF; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], fa[cur][i], fb[cur][j]);
+        for (int j = 0; j < NF; ++j) dmma(acc[i][j], fa[cur][i], fb[cur][j]);
     }
   }
   cp_async_wait<0>();
@@ -178,11 +190,177 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_task_kernel(const __grid_co
   // epilogue: C = alpha*acc + beta*C  (beta == 0: C never read)
   const double alpha = t.alpha, beta = t.beta;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < MF; ++i) {
     const int r = m0 + wm + i * 8 + g;
     if (r >= t.h) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = n0 + wn + j * 8 + 2 * q + e;
+        if (cc >= t.w) continue;
+        if (t.tri == TRI_LOWER && cc > r) continue;
+        if (t.tri == TRI_UPPER && cc < r) continue;
+        double* p = t.c + (size_t)cc * t.ldc + r;
+        double v = alpha * acc[i][j][e];
+        if (beta != 0.0) v = fma(beta, *p, v);
+        *p = v;
+      }
+    }
+  }
+}
+
+}  // namespace bx
+
+// ---------------------------------------------------------------------------------------
+// Barrier-free variant: every warp is both producer and consumer, but stage hand-off runs
+// through mbarriers instead of __syncthreads.  Each thread's cp.async share of a slab
+// arrives on the stage's "full" barrier when it lands (cp.async.mbarrier.arrive.noinc);
+// each warp releases a stage on its "empty" barrier after its fragment loads.  A warp
+// refills a stage only once every warp has finished the slab that lived there, which is
+// SLACK+1 slabs behind its own position, so warps drift freely and the FP64 tensor pipe
+// never drains at slab boundaries (the __syncthreads of the classic pipeline).
+// ---------------------------------------------------------------------------------------
+namespace bx {
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int SLACK_>
+struct MbCfg : GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_> {
+  using Base = GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_>;
+  static constexpr int SLACK = SLACK_;
+  static constexpr int DIST = STAGES_ - 1 - SLACK_;   // prefetch distance in slabs
+  static constexpr int WARPS = Base::WARPS_M * Base::WARPS_N;
+  static constexpr int SMEM_BYTES = Base::SMEM_BYTES + 2 * STAGES_ * 8;
+  static_assert(DIST >= 1, "stages");
+};
+
+using CfgMb = MbCfg<128, 128, 16, 64, 32, 5, 1>;    // default: 8 warps, 5-stage ring
+using CfgMb2 = MbCfg<128, 128, 16, 64, 32, 5, 2>;   // more slack, shorter prefetch
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <class Cfg, bool TA, bool TB>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_mb_kernel(const __grid_constant__ GemmTask t) {
+  extern __shared__ __align__(128) double smem[];
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES, DIST = Cfg::DIST;
+  constexpr int MF = Cfg::MF, NF = Cfg::NF, KQ = BK / 4;
+  constexpr bool A_KMAJ = TA;
+  constexpr bool B_KMAJ = !TB;
+  static_assert(KQ % 2 == 0, "fragment double buffer parity");
+
+  const int tiles_m = (t.h + BM - 1) / BM, tiles_n = (t.w + BN - 1) / BN;
+  const int bid = blockIdx.x;
+  const int per_group = t.group_m * tiles_n;
+  const int first_m = (bid / per_group) * t.group_m;
+  const int gsize = min(tiles_m - first_m, t.group_m);
+  const int bm = first_m + (bid % per_group) % gsize;
+  const int bn = (bid % per_group) / gsize;
+  const int m0 = bm * BM, n0 = bn * BN;
+  if (t.tri == TRI_LOWER && n0 >= m0 + BM) return;
+  if (t.tri == TRI_UPPER && m0 >= n0 + BN) return;
+
+  double* sA = smem;
+  double* sB = smem + STAGES * Cfg::A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_ELEMS);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], Cfg::THREADS);
+      mbar_init(&empty[s], Cfg::WARPS);
+    }
+  }
+  __syncthreads();
+
+  int total = 0;
+  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + BK - 1) / BK;
+
+  int ld_step = 0, ld_k = 0;
+  auto produce = [&](int slab) {
+    const int stage = slab % STAGES;
+    if (slab >= STAGES) mbar_wait(&empty[stage], ((slab / STAGES) - 1) & 1);
+    const GemmStep& st = t.steps[ld_step];
+    load_slab<Cfg, BM, A_KMAJ>(sA + stage * Cfg::A_ELEMS, st.a, st.lda, m0, t.h, ld_k, st.d, tid);
+    load_slab<Cfg, BN, B_KMAJ>(sB + stage * Cfg::B_ELEMS, st.b, st.ldb, n0, t.w, ld_k, st.d, tid);
+    cp_async_arrive_noinc(&full[stage]);
+    ld_k += BK;
+    if (ld_k >= st.d) { ld_k = 0; ++ld_step; }
+  };
+  for (int s = 0; s < DIST && s < total; ++s) produce(s);
+
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[MF][NF][2];
+#pragma unroll
+  for (int i = 0; i < MF; ++i)
+#pragma unroll
+    for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double fa[2][MF], fb[2][NF];
+  if (total > 0) {
+    mbar_wait(&full[0], 0);
+#pragma unroll
+    for (int i = 0; i < MF; ++i) fa[0][i] = frag<Cfg, BM, A_KMAJ>(sA, wm + i * 8 + g, q);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) fb[0][j] = frag<Cfg, BN, B_KMAJ>(sB, wn + j * 8 + g, q);
+  }
+  for (int it = 0; it < total; ++it) {
+    if (it + DIST < total) produce(it + DIST);
+    const int stage = it % STAGES;
+    const double* a = sA + stage * Cfg::A_ELEMS;
+    const double* b = sB + stage * Cfg::B_ELEMS;
+#pragma unroll
+    for (int kq = 0; kq < KQ; ++kq) {
+      const int cur = kq & 1, nx = cur ^ 1;
+      if (kq + 1 < KQ) {
+#pragma unroll
+        for (int i = 0; i < MF; ++i) fa[nx][i] = frag<Cfg, BM, A_KMAJ>(a, wm + i * 8 + g, (kq + 1) * 4 + q);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) fb[nx][j] = frag<Cfg, BN, B_KMAJ>(b, wn + j * 8 + g, (kq + 1) * 4 + q);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);   // this warp is done reading the stage
+        if (it + 1 < total) {
+          const int ns = (it + 1) % STAGES;
+          mbar_wait(&full[ns], ((it + 1) / STAGES) & 1);
+          const double* a2 = sA + ns * Cfg::A_ELEMS;
+          const double* b2 = sB + ns * Cfg::B_ELEMS;
+#pragma unroll
+          for (int i = 0; i < MF; ++i) fa[nx][i] = frag<Cfg, BM, A_KMAJ>(a2, wm + i * 8 + g, q);
+#pragma unroll
+          for (int j = 0; j < NF; ++j) fb[nx][j] = frag<Cfg, BN, B_KMAJ>(b2, wn + j * 8 + g, q);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) dmma(acc[i][j], fa[cur][i], fb[cur][j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const double alpha = t.alpha, beta = t.beta;
+#pragma unroll
+  for (int i = 0; i < MF; ++i) {
+    const int r = m0 + wm + i * 8 + g;
+    if (r >= t.h) continue;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = n0 + wn + j * 8 + 2 * q + e;

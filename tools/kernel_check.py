@@ -61,8 +61,28 @@ def gemm(ta, tb, tri, alpha, beta, A_list, B_list, c_arr):
     return get(oc, lc, h, w)
 
 
+variants = [0]
+for a in sys.argv:
+    if a.startswith("--variants="):
+        variants = [int(x) for x in a.split("=")[1].split(",")]
 rng = np.random.default_rng(1)
 fails = 0
+for var in variants:
+  lib.bx_set_gemm_variant(var)
+  for (h, w, d, ns) in [(13, 11, 10, 1), (200, 130, 77, 3), (257, 255, 33, 5)]:
+    for ta in (0, 1):
+        for tb in (0, 1):
+            _next[0] = 0
+            As = [rng.random((d, h) if ta else (h, d)) * 2 - 1 for _ in range(ns)]
+            Bs = [rng.random((w, d) if tb else (d, w)) * 2 - 1 for _ in range(ns)]
+            c = rng.random((h, w)) * 2 - 1
+            ref = sum((a.T if ta else a) @ (b.T if tb else b) for a, b in zip(As, Bs)) * 1.7 - 0.3 * c
+            out = gemm(ta, tb, 0, 1.7, -0.3, As, Bs, c)
+            err = np.abs(out - ref).max() / max(1.0, np.abs(ref).max())
+            if not err < 1e-13:
+                fails += 1
+                print("FAIL variant", var, h, w, d, ns, ta, tb, err)
+lib.bx_set_gemm_variant(variants[0])
 for (h, w, d, ns) in [(13, 11, 10, 1), (128, 128, 16, 1), (200, 130, 77, 3), (1024, 1024, 1024, 2), (257, 255, 33, 5)]:
     for ta in (0, 1):
         for tb in (0, 1):
@@ -128,11 +148,10 @@ for n, other in [(37, 29), (256, 100), (1024, 1024), (1500, 64)]:
                         print("FAIL trsm", n, other, side, uplo, trans, unit, err)
 print("kernel_check fails:", fails)
 
-if "--perf" in sys.argv:
-    tf = C.c_double()
-    N.check(lib.bx_fp64_peak_probe(0, 20000, C.byref(tf)))
-    print("dmma probe TF/s", tf.value)
-    for n in (4096, 8192, 16384):
+for var in (variants if "--perf" in sys.argv else []):
+    lib.bx_set_gemm_variant(var)
+    print("== variant", var)
+    for n in (8192, 16384):
         ptrs = []
         for _ in range(3):
             p = C.c_uint64()
