@@ -7,7 +7,9 @@ Numerics come from the oracle (tests may import it)."""
 
 from __future__ import annotations
 
+import functools
 import random
+import threading
 
 import numpy as np
 
@@ -16,7 +18,16 @@ from oracle import tiled as O
 LANES = (-1, -2, -3)
 
 
+def _locked(fn):
+    @functools.wraps(fn)
+    def wrap(self, *a, **kw):
+        with self._lock:
+            return fn(self, *a, **kw)
+    return wrap
+
+
 class FakeEngine:
+    """Thread-safe (the runtime's concurrent mode drives it from one thread per GPU)."""
     kind = "fake"
 
     def __init__(self, n_devices=1, seed=0, n_compute=4, arena_bytes=64 << 20):
@@ -33,6 +44,11 @@ class FakeEngine:
         self.registered = 0
         self.flag = [False] * n_devices
         self.ops_log = []
+        self._lock = threading.RLock()
+        for name in ("ensure_arenas", "register_host", "unregister_host", "h2d", "d2h", "p2p",
+                     "gemm", "trsm", "materialize", "singular", "record", "done", "wait_any",
+                     "sync", "stream_wait", "device_sync"):
+            setattr(self, name, _locked(getattr(type(self), name)).__get__(self))
 
     # ---- devices ----
     def slot(self, cuda_id):
