@@ -1,0 +1,114 @@
+"""Compile a planner Task into the launch program the GPU runtime issues.
+
+Data only (no device state): consecutive tile steps that share a kernel configuration
+are fused into one GEMM launch of up to ``chunk_steps`` sub-steps (accumulators stay in
+registers across them); rank-k diagonal steps become triangle-epilogue GEMMs; SYRK
+diagonal steps pair a tile with its own transpose, SYR2K diagonal steps expand into the
+two products alpha(A B^T + B A^T) (kernels.py:67-102); TRMM / SYMM diagonal steps first
+materialise op(tri(A)) / sym(A) into a scratch tile (kernels.py:164-211); TRSM ends with
+the triangular solve (kernels.py:105-161).  Programs depend only on the task structure,
+so they are cached on the (immutable) Task.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
+                       TRSM_SOLVE, Task)
+
+
+class GemmOp(NamedTuple):
+    ta: bool
+    tb: bool
+    tri: int             # 0 full, 1 lower, 2 upper
+    alpha: float
+    beta: float
+    subs: tuple          # ((a_key, b_key, depth), ...)
+    k: int
+    flops: int
+
+
+class MatOp(NamedTuple):
+    sym: bool
+    key: tuple           # diagonal tile key
+    n: int
+    scratch: int         # scratch slot index
+
+
+class TrsmOp(NamedTuple):
+    key: tuple
+    alpha: float
+    k: int
+    flops: int
+
+
+class Program(NamedTuple):
+    ops: tuple
+    scratch_n: tuple     # order of each scratch tile
+
+
+def scratch_key(i: int) -> tuple:
+    return ("#scratch", i)
+
+
+def compile_task(task: Task, call, chunk_steps: int) -> Program:
+    cache = getattr(task, "_bx_prog", None)
+    if cache is not None and cache[0] == chunk_steps:
+        return cache[1]
+    h, w = task.out_ref.phys_height, task.out_ref.phys_width
+    tri = 1 if call.uplo == "lower" else 2
+    ops = []
+    scratch = []
+    cur = None          # [ta, tb, tri, alpha, beta, subs, k]
+
+    def flush():
+        nonlocal cur
+        if cur is not None:
+            subs = tuple(cur[5])
+            ops.append(GemmOp(cur[0], cur[1], cur[2], cur[3], cur[4], subs, cur[6],
+                              sum(2 * h * w * d for _, _, d in subs)))
+            cur = None
+
+    def add(ta, tb, tr, alpha, beta, a, b, d, k):
+        nonlocal cur
+        if (cur is None or (cur[0], cur[1], cur[2], cur[3]) != (ta, tb, tr, alpha)
+                or beta != 1.0 or len(cur[5]) >= chunk_steps):
+            flush()
+            cur = [ta, tb, tr, alpha, beta, [], k]
+        cur[5].append((a, b, d))
+
+    for st in task.steps:
+        kind = st.kind
+        if kind == GEMM_UPDATE:
+            add(st.a.transposed, st.b.transposed, 0, st.alpha, st.beta, st.a.key(), st.b.key(),
+                st.a.width, st.k)
+        elif kind == SYRK_UPDATE:
+            ka = st.a.key()
+            add(st.a.transposed, not st.a.transposed, tri, st.alpha, st.beta, ka, ka,
+                st.a.width, st.k)
+        elif kind == SYR2K_UPDATE:
+            ka, kb = st.a.key(), st.b.key()
+            add(st.a.transposed, not st.b.transposed, tri, st.alpha, st.beta, ka, kb,
+                st.a.width, st.k)
+            add(st.b.transposed, not st.a.transposed, tri, st.alpha, 1.0, kb, ka,
+                st.a.width, st.k)
+        elif kind in (TRMM_DIAG, SYMM_DIAG):
+            n = st.a.phys_height
+            idx = len(scratch)
+            scratch.append(n)
+            ops.append(MatOp(kind == SYMM_DIAG, st.a.key(), n, idx))
+            sk = scratch_key(idx)
+            if call.side == "left":
+                add(False, st.b.transposed, 0, st.alpha, st.beta, sk, st.b.key(), n, st.k)
+            else:
+                add(st.b.transposed, False, 0, st.alpha, st.beta, st.b.key(), sk, n, st.k)
+        elif kind == TRSM_SOLVE:
+            flush()
+            ops.append(TrsmOp(st.a.key(), st.alpha, st.k, st.flops))
+        else:
+            raise ValueError(f"unknown step kind {kind!r}")
+    flush()
+    prog = Program(tuple(ops), tuple(scratch))
+    task._bx_prog = (chunk_steps, prog)
+    return prog

@@ -200,71 +200,83 @@ def validate(call: RoutineCall) -> None:
 # Each planner yields (k, kind, a_ref, b_ref, depth) for output tile (i, j); the scalar
 # policy (alpha/beta per step) is applied by ``_scalars``.
 
+_TR_MEMO = {}
+
+
+def _tr(ref: TileRef) -> TileRef:
+    out = _TR_MEMO.get(ref)
+    if out is None:
+        if len(_TR_MEMO) > 1 << 16:
+            _TR_MEMO.clear()
+        out = _TR_MEMO[ref] = transpose_ref(ref)
+    return out
+
+
 def _k_tiles(tm: TiledMatrix, trans: bool) -> int:
     return tm.tile_rows if trans else tm.tile_cols
 
 
-def _gemm_steps(call, i, j, _snap):
+def _gemm_steps(call, i, j, _snap, lt):
     for k in range(_k_tiles(call.a, call.trans_a)):
-        a = logical_tile(call.a, i, k, call.trans_a)
-        yield k, GEMM_UPDATE, a, logical_tile(call.b, k, j, call.trans_b), a.width
+        a = lt(call.a, i, k, call.trans_a)
+        yield k, GEMM_UPDATE, a, lt(call.b, k, j, call.trans_b), a.width
 
 
-def _syrk_steps(call, i, j, _snap):
+def _syrk_steps(call, i, j, _snap, lt):
     ta = call.trans_a
     for k in range(_k_tiles(call.a, ta)):
-        a = logical_tile(call.a, i, k, ta)
+        a = lt(call.a, i, k, ta)
         if i == j:
             yield k, SYRK_UPDATE, a, None, a.width
         else:
-            yield k, GEMM_UPDATE, a, transpose_ref(logical_tile(call.a, j, k, ta)), a.width
+            yield k, GEMM_UPDATE, a, _tr(lt(call.a, j, k, ta)), a.width
 
 
-def _syr2k_steps(call, i, j, _snap):
+def _syr2k_steps(call, i, j, _snap, lt):
     ta = call.trans_a
     for k in range(_k_tiles(call.a, ta)):
-        a = logical_tile(call.a, i, k, ta)
-        b = logical_tile(call.b, i, k, ta)
+        a = lt(call.a, i, k, ta)
+        b = lt(call.b, i, k, ta)
         if i == j:
             yield k, SYR2K_UPDATE, a, b, a.width
         else:
-            yield k, GEMM_UPDATE, a, transpose_ref(logical_tile(call.b, j, k, ta)), a.width
-            yield k, GEMM_UPDATE, b, transpose_ref(logical_tile(call.a, j, k, ta)), b.width
+            yield k, GEMM_UPDATE, a, _tr(lt(call.b, j, k, ta)), a.width
+            yield k, GEMM_UPDATE, b, _tr(lt(call.a, j, k, ta)), b.width
 
 
-def _sym_tile(call, r, c) -> TileRef:
+def _sym_tile(call, r, c, lt) -> TileRef:
     """Tile (r, c) of the symmetric extension of the stored triangle (routines.py:279-284)."""
     in_stored = c > r if call.uplo == "upper" else c < r
     if in_stored:
-        return logical_tile(call.a, r, c, False)
-    return transpose_ref(logical_tile(call.a, c, r, False))
+        return lt(call.a, r, c, False)
+    return _tr(lt(call.a, c, r, False))
 
 
-def _symm_steps(call, i, j, _snap):
+def _symm_steps(call, i, j, _snap, lt):
     left = call.side == "left"
     for k in range(call.a.tile_rows):
         if left:
-            b = logical_tile(call.b, k, j, False)
+            b = lt(call.b, k, j, False)
             if k == i:
-                d = logical_tile(call.a, i, i, False)
+                d = lt(call.a, i, i, False)
                 yield k, SYMM_DIAG, d, b, d.height
             else:
-                a = _sym_tile(call, i, k)
+                a = _sym_tile(call, i, k, lt)
                 yield k, GEMM_UPDATE, a, b, a.width
         else:
-            a = logical_tile(call.b, i, k, False)
+            a = lt(call.b, i, k, False)
             if k == j:
-                d = logical_tile(call.a, j, j, False)
+                d = lt(call.a, j, j, False)
                 yield k, SYMM_DIAG, d, a, d.height
             else:
-                yield k, GEMM_UPDATE, a, _sym_tile(call, k, j), a.width
+                yield k, GEMM_UPDATE, a, _sym_tile(call, k, j, lt), a.width
 
 
 def _eff_upper(call) -> bool:
     return (call.uplo == "upper") != call.trans_a
 
 
-def _trmm_steps(call, i, j, snap):
+def _trmm_steps(call, i, j, snap, lt):
     nt = call.a.tile_rows
     if call.side == "left":
         diag_k = i
@@ -274,14 +286,14 @@ def _trmm_steps(call, i, j, snap):
         ks = range(j + 1) if _eff_upper(call) else range(j, nt)
     for k in ks:
         if k == diag_k:
-            d = logical_tile(call.a, k, k, False)
-            yield k, TRMM_DIAG, d, logical_tile(snap, i, j, False), d.height
+            d = lt(call.a, k, k, False)
+            yield k, TRMM_DIAG, d, lt(snap, i, j, False), d.height
         elif call.side == "left":
-            a = logical_tile(call.a, i, k, call.trans_a)
-            yield k, GEMM_UPDATE, a, logical_tile(snap, k, j, False), a.width
+            a = lt(call.a, i, k, call.trans_a)
+            yield k, GEMM_UPDATE, a, lt(snap, k, j, False), a.width
         else:
-            s = logical_tile(snap, i, k, False)
-            yield k, GEMM_UPDATE, s, logical_tile(call.a, k, j, call.trans_a), s.width
+            s = lt(snap, i, k, False)
+            yield k, GEMM_UPDATE, s, lt(call.a, k, j, call.trans_a), s.width
 
 
 def trsm_producers(call, i: int, j: int) -> range:
@@ -292,16 +304,16 @@ def trsm_producers(call, i: int, j: int) -> range:
     return range(j) if _eff_upper(call) else range(j + 1, nt)
 
 
-def _trsm_steps(call, i, j, _snap):
+def _trsm_steps(call, i, j, _snap, lt):
     for k in trsm_producers(call, i, j):
         if call.side == "left":
-            a = logical_tile(call.a, i, k, call.trans_a)
-            yield k, GEMM_UPDATE, a, logical_tile(call.c, k, j, False), a.width
+            a = lt(call.a, i, k, call.trans_a)
+            yield k, GEMM_UPDATE, a, lt(call.c, k, j, False), a.width
         else:
-            x = logical_tile(call.c, i, k, False)
-            yield k, GEMM_UPDATE, x, logical_tile(call.a, k, j, call.trans_a), x.width
+            x = lt(call.c, i, k, False)
+            yield k, GEMM_UPDATE, x, lt(call.a, k, j, call.trans_a), x.width
     dk = i if call.side == "left" else j
-    d = logical_tile(call.a, dk, dk, False)
+    d = lt(call.a, dk, dk, False)
     yield dk, TRSM_SOLVE, d, None, d.height
 
 
@@ -339,8 +351,26 @@ def _output_pairs(call):
     return [(i, j) for i in range(mt) for j in range(nt)]
 
 
-def generate_tasks(call: RoutineCall) -> TaskPlan:
-    """Expand a call into its task plan (reference routines.py:383-441)."""
+_PLAN_CACHE = {}
+_PLAN_CACHE_MAX = 8
+
+
+def _structure_key(call: RoutineCall) -> tuple:
+    """Everything a plan's task structure depends on (shapes, tiling, flags, scalars and
+    matrix ids) — but not the operand values or storage."""
+    def shape(tm):
+        return None if tm is None else (tm.matrix_id, tm.matrix.rows, tm.matrix.cols)
+    return (call.kind, shape(call.a), shape(call.b), shape(call.c), call.c.tile_size,
+            call.alpha, call.beta, call.trans_a, call.trans_b, call.uplo, call.side, call.diag,
+            str(call.c.matrix.storage.dtype))
+
+
+def generate_tasks(call: RoutineCall, cache: bool = True) -> TaskPlan:
+    """Expand a call into its task plan (reference routines.py:383-441).
+
+    The task structure is a pure function of shapes / flags / scalars, so it is memoised
+    (``cache``): a repeated call of the same shape rebinds the cached tasks to the new
+    operand storage instead of re-planning."""
     validate(call)
     t = call.c.tile_size
     matrices = {tm.matrix_id: tm.matrix for tm in (call.a, call.c, call.b) if tm is not None}
@@ -351,14 +381,28 @@ def generate_tasks(call: RoutineCall) -> TaskPlan:
                         src.storage.copy(), src.base_offset)
         snap = TiledMatrix(sd, t, call.c.tile_rows, call.c.tile_cols)
         matrices[sd.matrix_id] = sd
+    skey = _structure_key(call) if cache else None
+    hit = _PLAN_CACHE.get(skey) if cache else None
+    if hit is not None:
+        tasks, total = hit
+        return TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
     planner = _PLANNERS[call.kind]
+    memo = {}
+
+    def lt(tm, i, j, trans=False):
+        # every input tile is referenced by many tasks: build each TileRef once per plan
+        key = (tm.matrix_id, i, j, trans)
+        ref = memo.get(key)
+        if ref is None:
+            ref = memo[key] = logical_tile(tm, i, j, trans)
+        return ref
     pairs = sorted(_output_pairs(call), key=lambda p: morton_key(*p))
     tasks = []
     for tid, (i, j) in enumerate(pairs):
         out = logical_tile(call.c, i, j, False)
         steps = []
         n_gemm = 0
-        for idx, (k, kind, a, b, d) in enumerate(planner(call, i, j, snap)):
+        for idx, (k, kind, a, b, d) in enumerate(planner(call, i, j, snap, lt)):
             alpha, beta = _scalars(call, idx, kind, n_gemm)
             n_gemm += kind == GEMM_UPDATE
             steps.append(TaskStep(k, kind, a, b, alpha, beta,
@@ -376,8 +420,12 @@ def generate_tasks(call: RoutineCall) -> TaskPlan:
                 deps[prod.task_id].append(x.task_id)
         for x in tasks:
             x.dependents = tuple(sorted(deps[x.task_id]))
-    return TaskPlan(call, t, tasks, matrices, sum(x.flops for x in tasks),
-                    call.c.matrix.storage.dtype)
+    total = sum(x.flops for x in tasks)
+    if cache:
+        if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+        _PLAN_CACHE[skey] = (tasks, total)
+    return TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
 
 
 def gemm_flop_fraction(plan: TaskPlan) -> float:

@@ -42,6 +42,7 @@ from .errors import CapacityDeadlockError, ConfigError, SingularMatrixError
 from .memory import Arena
 from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
                        TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
+from .program import GemmOp, MatOp, compile_task, scratch_key
 from .tiling import device_ld
 
 WORKING_SET_TILES = 12   # reference floor (scheduler.py:49-52): 4 tasks x (C + 2 inputs)
@@ -75,7 +76,8 @@ class RunOptions:
     l2_enabled: bool = True
     record_trace: bool = False
     n_streams: int = 4
-    chunk_steps: int = 8               # k-steps fused per kernel launch
+    chunk_steps: int = 16              # k-steps fused per kernel launch
+    tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -193,21 +195,10 @@ class _Runtime:
             self.trace.append(ev)
 
 
-class _Chunk:
-    """Consecutive gemm sub-steps fused into one kernel launch."""
-    __slots__ = ("ta", "tb", "tri", "alpha", "beta", "steps", "waits", "k")
-
-    def __init__(self, ta, tb, tri, alpha, beta, k):
-        self.ta, self.tb, self.tri, self.alpha, self.beta, self.k = ta, tb, tri, alpha, beta, k
-        self.steps = []
-        self.waits = []
-
-
 class _Active:
     """A task in flight on one compute stream."""
     __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
-                 "events", "last_ev", "done_ev", "chunk", "pending_waits", "flops",
-                 "trace_evs")
+                 "events", "last_ev", "done_ev", "pending_waits", "flops")
 
     def __init__(self, entry, stream):
         self.entry = entry
@@ -220,10 +211,8 @@ class _Active:
         self.events = []         # event ids owned by the task
         self.last_ev = None      # event after the last kernel
         self.done_ev = None      # write-back completion
-        self.chunk = None
         self.pending_waits = []  # waits to attach to the next launch (C move-in)
         self.flops = 0
-        self.trace_evs = []      # (kind, lane, ev0, ev1, nbytes_or_flops, k)
 
 
 class _GpuWorker:
@@ -243,7 +232,10 @@ class _GpuWorker:
                                      l2_enabled=opts.l2_enabled, on_evict=self._on_evict)
         self.rs = ReservationStation(desc.device_id, opts.rs_capacity)
         self.dm = runtime.device_metrics[desc.device_id]
-        self.active = [None] * opts.n_streams
+        # active slots: tasks_per_stream tasks may be queued on each compute stream, so the
+        # next task's copies and kernels are already enqueued when the current one drains
+        self.n_streams = opts.n_streams
+        self.active = [None] * (opts.n_streams * opts.tasks_per_stream)
         self.l1_hits = self.l2_hits = self.host_fetches = 0
         self.tasks_done = 0
         self._cur: Optional[_Active] = None
@@ -252,6 +244,10 @@ class _GpuWorker:
         self.tile = runtime.plan.tile_size
         self.trace_on = opts.record_trace
         self.epoch = None
+        grp = runtime.topology.peer_group_of(desc)
+        self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
+                                      if d.device_id != desc.device_id
+                                      and runtime.topology.peer_group_of(d) == grp)
 
     # ---- cache callbacks ------------------------------------------------------------
 
@@ -313,8 +309,6 @@ class _GpuWorker:
         """Every cached block is pinned: launch what is pending, drain the GPU, release the
         pins of all launched work and retire finished tasks, then let the caller retry."""
         cur = self._cur
-        if cur is not None and cur.chunk is not None:
-            self._flush(cur)
         self.eng.device_sync(self.slot)
         for act in [a for a in self.active if a is not None] + ([cur] if cur else []):
             for cache, blk in act.launched_pins:
@@ -346,17 +340,19 @@ class _GpuWorker:
                 self.rs.put(stolen)
 
     def _priority(self, task: Task) -> int:
-        contains = self.cache.contains
-        peer = self.runtime.directory.peer_source
-        l2 = self.runtime.options.l2_enabled
+        """Eq. 3: +2 per input-tile reference already in this GPU's L1, +1 per reference
+        held by a peer of the same group (counted per step reference, scheduler.py:341-354)."""
+        blocks = self.cache._blocks
+        holders = self.runtime.directory._holders if self.runtime.options.l2_enabled else None
+        group = self._group_peers
         p = 0
-        for step in task.steps:
-            for ref in step.input_refs():
-                key = ref.key()
-                if contains(key):
-                    p += 2
-                elif l2 and peer(key, self.device_id) is not None:
-                    p += 1
+        for key, (_ref, mult) in task_keys(task).items():
+            if key in blocks:
+                p += 2 * mult
+            elif holders is not None:
+                held = holders.get(key)
+                if held and not group.isdisjoint(held):
+                    p += mult
         return p
 
     def _next_entry(self):
@@ -379,11 +375,59 @@ class _GpuWorker:
 
     # ---- issue ----------------------------------------------------------------------
 
+    def _resolve_task(self, task):
+        """Translate every distinct input tile of a task once (L1 hit / L2 peer copy / host
+        fetch), pin it once for the task, and return key -> (offset, ld, wait).  Hit/miss
+        counters follow the per-reference semantics of the reference translate loop."""
+        act = self._cur
+        out = {}
+        cache = self.cache
+        blocks = cache._blocks
+        for key, (ref, mult) in task_keys(task).items():
+            with cache.lock:
+                blk = blocks.get(key)
+                if blk is not None:
+                    blocks.move_to_end(key)
+                    blk.reader += 1
+            if blk is not None:
+                self.l1_hits += mult
+            else:
+                h, w, ld, nbytes = self._tile_geom(ref)
+                blk, outcome = cache.translate(ref, self, nbytes=nbytes, ld=ld)
+                if outcome == L1_HIT:
+                    self.l1_hits += mult
+                else:
+                    if outcome == L2_HIT:
+                        self.l2_hits += 1
+                    else:
+                        self.host_fetches += 1
+                    self.l1_hits += mult - 1
+                cache.pin(blk)
+            act.pins.append((cache, blk))
+            wait = None
+            if blk.ready_ev is not None and not blk.ready_done:
+                if self.eng.done(blk.ready_ev):
+                    blk.ready_done = True
+                else:
+                    wait = blk.ready_ev
+            out[key] = (blk.offset, blk.ld, wait)
+        return out
+
+    def _resolve_uncached(self, task):
+        """l1_enabled=False (scheduler.py:463-485): every step reference is a fresh host
+        fetch into a transient buffer; a tile referenced by several steps of the task is
+        fetched once per reference (counted as such) and the last copy is used."""
+        out = {}
+        for st in task.steps:
+            for ref in st.input_refs():
+                out[ref.key()] = self._resolve(ref)
+        return out
+
     def _resolve(self, ref):
-        """Translate + pin one input tile; returns (offset, ld, arrival-wait or None)."""
+        """Uncached path (l1_enabled=False): every reference is a fresh host fetch."""
         act = self._cur
         h, w, ld, nbytes = self._tile_geom(ref)
-        if not self.runtime.options.l1_enabled:
+        if True:
             off = self.cache.allocate_under_pressure(nbytes, self)
             act.scratch.append(off)
             desc, r0, c0 = self._host_of(ref)
@@ -393,50 +437,6 @@ class _GpuWorker:
             self.dm.h2d_bytes += h * w * self.esz
             self.host_fetches += 1
             return off, ld, ev
-        blk, outcome = self.cache.translate(ref, self, nbytes=nbytes, ld=ld)
-        if outcome == L1_HIT:
-            self.l1_hits += 1
-        elif outcome == L2_HIT:
-            self.l2_hits += 1
-        else:
-            self.host_fetches += 1
-        self.cache.pin(blk)
-        act.pins.append((self.cache, blk))
-        wait = None
-        if blk.ready_ev is not None and not blk.ready_done:
-            if self.eng.done(blk.ready_ev):
-                blk.ready_done = True
-            else:
-                wait = blk.ready_ev
-        return blk.offset, blk.ld, wait
-
-    def _add_sub(self, act, ta, tb, tri, alpha, beta, a, b, depth, k):
-        ch = act.chunk
-        max_steps = self.runtime.options.chunk_steps
-        if (ch is None or (ch.ta, ch.tb, ch.tri, ch.alpha) != (ta, tb, tri, alpha)
-                or beta != 1.0 or len(ch.steps) >= max_steps):
-            if ch is not None:
-                self._flush(act)
-            ch = act.chunk = _Chunk(ta, tb, tri, alpha, beta, k)
-        ch.steps.append((a[0], a[1], b[0], b[1], depth))
-        for wv in (a[2], b[2]):
-            if wv is not None and wv not in ch.waits:
-                ch.waits.append(wv)
-
-    def _flush(self, act) -> None:
-        ch = act.chunk
-        if ch is None:
-            return
-        act.chunk = None
-        task = act.entry.task
-        h, w = task.out_ref.phys_height, task.out_ref.phys_width
-        waits = ch.waits + act.pending_waits
-        act.pending_waits = []
-        flops = sum(2 * h * w * s[4] for s in ch.steps)
-        ev = self._timed(act.stream, lambda wt: self.eng.gemm(
-            self.slot, act.stream, ch.ta, ch.tb, ch.tri, h, w, ch.steps, ch.alpha, ch.beta,
-            act.c_off, act.c_ld, wt), waits, "KERNEL", flops, ch.k)
-        self._launched(act, ev)
 
     def _launched(self, act, ev) -> None:
         act.events.append(ev)
@@ -445,17 +445,15 @@ class _GpuWorker:
         act.pins = []
         self.dm.kernel_launches += 1
 
-    def _scratch_tile(self, act, n):
-        ld = device_ld(n)
-        off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
-        act.scratch.append(off)
-        return off, ld
-
     def _issue(self, entry, stream) -> None:
         task = entry.task
         call = self.plan.call
+        opts = self.runtime.options
+        slot_index = stream
+        stream = stream % self.n_streams
         act = _Active(entry, stream)
         self._cur = act
+        eng, slot = self.eng, self.slot
         try:
             out = task.out_ref
             h, w = out.phys_height, out.phys_width
@@ -463,76 +461,69 @@ class _GpuWorker:
             act.c_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
             if task.needs_c_move_in:
                 desc, r0, c0 = self._host_of(out)
-                ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(
-                    self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
+                ev = self._timed(LANE_H2D, lambda wt: eng.h2d(
+                    slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
                     h * w * self.esz)
                 act.events.append(ev)
                 act.pending_waits.append(ev)
                 self.dm.h2d_bytes += h * w * self.esz
-            tri_mode = 1 if call.uplo == "lower" else 2
-            for st in task.steps:
-                kind = st.kind
-                if kind == GEMM_UPDATE:
-                    a = self._resolve(st.a)
-                    b = self._resolve(st.b)
-                    self._add_sub(act, st.a.transposed, st.b.transposed, 0, st.alpha, st.beta,
-                                  a, b, st.a.width, st.k)
-                elif kind == SYRK_UPDATE:
-                    a = self._resolve(st.a)
-                    self._add_sub(act, st.a.transposed, not st.a.transposed, tri_mode, st.alpha,
-                                  st.beta, a, a, st.a.width, st.k)
-                elif kind == SYR2K_UPDATE:
-                    a = self._resolve(st.a)
-                    b = self._resolve(st.b)
-                    self._add_sub(act, st.a.transposed, not st.b.transposed, tri_mode, st.alpha,
-                                  st.beta, a, b, st.a.width, st.k)
-                    self._add_sub(act, st.b.transposed, not st.a.transposed, tri_mode, st.alpha,
-                                  1.0, b, a, st.a.width, st.k)
-                elif kind in (TRMM_DIAG, SYMM_DIAG):
-                    a = self._resolve(st.a)
-                    b = self._resolve(st.b)
-                    n = st.a.phys_height
-                    s_off, s_ld = self._scratch_tile(act, n)
-                    sym = kind == SYMM_DIAG
-                    waits = [a[2]] if a[2] is not None else []
-                    ev = self._timed(stream, lambda wt: self.eng.materialize(
-                        self.slot, stream, sym, call.uplo == "upper",
-                        False if sym else call.trans_a, (not sym) and call.diag == "unit", n,
-                        a[0], a[1], s_off, s_ld, wt), waits, "KERNEL", 0, st.k)
-                    act.events.append(ev)
-                    scratch = (s_off, s_ld, None)
-                    if call.side == "left":
-                        self._add_sub(act, False, st.b.transposed, 0, st.alpha, st.beta,
-                                      scratch, b, n, st.k)
-                    else:
-                        self._add_sub(act, st.b.transposed, False, 0, st.alpha, st.beta,
-                                      b, scratch, n, st.k)
-                elif kind == TRSM_SOLVE:
-                    a = self._resolve(st.a)
-                    self._flush(act)
-                    waits = ([a[2]] if a[2] is not None else []) + act.pending_waits
+            prog = compile_task(task, call, opts.chunk_steps)
+            if opts.l1_enabled:
+                res = self._resolve_task(task)
+            else:
+                res = self._resolve_uncached(task)
+            for i, n in enumerate(prog.scratch_n):
+                ld = device_ld(n)
+                off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
+                act.scratch.append(off)
+                res[scratch_key(i)] = (off, ld, None)
+            for op in prog.ops:
+                if type(op) is GemmOp:
+                    steps = []
+                    waits = []
+                    for ak, bk, d in op.subs:
+                        ao, al, aw = res[ak]
+                        bo, bl, bw = res[bk]
+                        steps.append((ao, al, bo, bl, d))
+                        if aw is not None and aw not in waits:
+                            waits.append(aw)
+                        if bw is not None and bw not in waits:
+                            waits.append(bw)
+                    waits += act.pending_waits
                     act.pending_waits = []
-                    flops = st.flops
-                    ev = self._timed(stream, lambda wt: self.eng.trsm(
-                        self.slot, stream, call.side == "right", call.uplo == "upper",
-                        call.trans_a, call.diag == "unit", h, w, st.alpha, a[0], a[1],
-                        act.c_off, act.c_ld, wt), waits, "KERNEL", flops, st.k)
+                    ev = self._timed(stream, lambda wt, op=op, steps=steps: eng.gemm(
+                        slot, stream, op.ta, op.tb, op.tri, h, w, steps, op.alpha, op.beta,
+                        act.c_off, act.c_ld, wt), waits, "KERNEL", op.flops, op.k)
                     self._launched(act, ev)
-                else:
-                    raise ConfigError(f"unknown step kind {kind!r}")
-            self._flush(act)
+                elif type(op) is MatOp:
+                    ao, al, aw = res[op.key]
+                    so, sl, _ = res[scratch_key(op.scratch)]
+                    ev = self._timed(stream, lambda wt, op=op, ao=ao, al=al, so=so, sl=sl: eng.materialize(
+                        slot, stream, op.sym, call.uplo == "upper",
+                        False if op.sym else call.trans_a, (not op.sym) and call.diag == "unit",
+                        op.n, ao, al, so, sl, wt), [aw] if aw is not None else [], "KERNEL", 0, -1)
+                    act.events.append(ev)
+                else:   # TrsmOp
+                    ao, al, aw = res[op.key]
+                    waits = ([aw] if aw is not None else []) + act.pending_waits
+                    act.pending_waits = []
+                    ev = self._timed(stream, lambda wt, op=op, ao=ao, al=al: eng.trsm(
+                        slot, stream, call.side == "right", call.uplo == "upper", call.trans_a,
+                        call.diag == "unit", h, w, op.alpha, ao, al, act.c_off, act.c_ld, wt),
+                        waits, "KERNEL", op.flops, op.k)
+                    self._launched(act, ev)
             desc, r0, c0 = self._host_of(out)
             waits = [act.last_ev] + act.pending_waits
             act.pending_waits = []
-            act.done_ev = self._timed(LANE_D2H, lambda wt: self.eng.d2h(
-                self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), waits, "D2H",
+            act.done_ev = self._timed(LANE_D2H, lambda wt: eng.d2h(
+                slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), waits, "D2H",
                 h * w * self.esz)
             self.dm.d2h_bytes += h * w * self.esz
             act.events.append(act.done_ev)
             act.flops = task.flops
         finally:
             self._cur = None
-        self.active[stream] = act
+        self.active[slot_index] = act
 
     # ---- completion -----------------------------------------------------------------
 
@@ -578,20 +569,37 @@ class _GpuWorker:
             self._on_evict(blk)
 
 
+def task_keys(task: Task) -> dict:
+    """Distinct input tiles of a task: key -> (ref, number of step references).  Cached on
+    the (immutable) task."""
+    keys = getattr(task, "_bx_keys", None)
+    if keys is None:
+        keys = {}
+        for st in task.steps:
+            for ref in st.input_refs():
+                k = ref.key()
+                hit = keys.get(k)
+                keys[k] = (ref if hit is None else hit[0], 1 if hit is None else hit[1] + 1)
+        task._bx_keys = keys
+    return keys
+
+
 def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: int) -> int:
-    """Enough for every distinct input tile plus the in-flight C / scratch buffers,
+    """Enough for every tile of every input matrix plus the in-flight C / scratch buffers,
     capped at 90 % of free HBM (no eviction at BASELINE sizes on a 180 GB B200)."""
     esz = plan.dtype.itemsize
     t = plan.tile_size
-    seen = {}
-    for task in plan.tasks:
-        for st in task.steps:
-            for ref in st.input_refs():
-                if ref.key() not in seen:
-                    seen[ref.key()] = device_ld(ref.phys_height) * ref.phys_width * esz
+    out_id = plan.call.c.matrix_id
+    want = 0
+    for mid, m in plan.matrices.items():
+        if mid == out_id and plan.call.kind != "trsm":
+            continue           # output tiles bypass the cache (except TRSM's solved tiles)
+        rows_full, rem = divmod(m.rows, t)
+        col_tiles = -(-m.cols // t)
+        per_col_tile = rows_full * device_ld(t) + (device_ld(rem) if rem else 0)
+        want += -(-per_col_tile * t * col_tiles * esz // 256) * 256 + 256 * col_tiles * (rows_full + 1)
     per_tile = device_ld(t) * t * esz
-    want = sum(-(-v // 256) * 256 for v in seen.values())
-    want += (options.n_streams + 2) * 2 * per_tile + (64 << 20)
+    want += (options.n_streams * options.tasks_per_stream + 2) * 2 * per_tile + (64 << 20)
     cap = int(free_bytes * 0.9) - (1 << 30)
     return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
 
@@ -607,6 +615,8 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         raise ConfigError("n_streams must be in 1..8")
     if options.chunk_steps < 1:
         raise ConfigError("chunk_steps must be >= 1")
+    if options.tasks_per_stream < 1:
+        raise ConfigError("tasks_per_stream must be >= 1")
     topology = topology or discover_topology()
     devs = topology.accelerators()
     if engine is None:

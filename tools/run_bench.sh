@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 1500 python bench.py "$@" > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
