@@ -180,6 +180,9 @@ int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
     case 1: return launch_gemm_cfg<bx::CfgWide, TA, TB>(t, s, 1u << (16 + tb));
     case 2: return launch_gemm_cfg<bx::CfgDeep, TA, TB>(t, s, 1u << (24 + tb));
     case 3: return launch_gemm_ws<bx::CfgMb2, TA, TB>(t, s, 1u << (20 + tb));
+    case 4: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s, 1u << (28 + tb));
+    case 5: return launch_gemm_ws<bx::CfgMbPair, TA, TB>(t, s, 1u << (4 + tb));
+    case 6: return launch_gemm_ws<bx::CfgMbPairS, TA, TB>(t, s, 1u << (0 + tb));
     default: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s, 1u << (12 + tb));
   }
 }

@@ -223,10 +223,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_kernel(const __grid
 // ---------------------------------------------------------------------------------------
 namespace bx {
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int SLACK_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int SLACK_, int MINB_ = 1>
 struct MbCfg : GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_> {
   using Base = GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_>;
   static constexpr int SLACK = SLACK_;
+  static constexpr int MIN_BLOCKS = MINB_;   // CTAs per SM the register budget targets
   static constexpr int DIST = STAGES_ - 1 - SLACK_;   // prefetch distance in slabs
   static constexpr int WARPS = Base::WARPS_M * Base::WARPS_N;
   static constexpr int SMEM_BYTES = Base::SMEM_BYTES + 2 * STAGES_ * 8;
@@ -235,6 +236,10 @@ struct MbCfg : GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_> {
 
 using CfgMb = MbCfg<128, 128, 16, 64, 32, 5, 1>;    // default: 8 warps, 5-stage ring
 using CfgMb2 = MbCfg<128, 128, 16, 64, 32, 5, 2>;   // more slack, shorter prefetch
+using CfgMb16 = MbCfg<128, 128, 16, 32, 32, 5, 1>;  // 16 warps (4 per SMSP)
+// two CTAs per SM (4 warps each): one CTA's stage hand-offs hide behind the other's DMMAs
+using CfgMbPair = MbCfg<64, 128, 16, 32, 64, 3, 0, 2>;
+using CfgMbPairS = MbCfg<64, 128, 16, 32, 64, 3, 1, 2>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -254,7 +259,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
 }
 
 template <class Cfg, bool TA, bool TB>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_mb_kernel(const __grid_constant__ GemmTask t) {
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_kernel(const __grid_constant__ GemmTask t) {
   extern __shared__ __align__(128) double smem[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES, DIST = Cfg::DIST;
   constexpr int MF = Cfg::MF, NF = Cfg::NF, KQ = BK / 4;

@@ -1,0 +1,7 @@
+import torch
+n = 8192
+a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+for _ in range(2):
+    c = a @ b
+torch.cuda.synchronize()
