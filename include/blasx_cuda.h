@@ -52,6 +52,8 @@ int bx_device_count(int* n);
 /* name (>=64 bytes), SM count, total and free HBM bytes */
 int bx_device_info(int dev, char* name, int name_len, int* sms, uint64_t* total_bytes,
                    uint64_t* free_bytes);
+/* free / total HBM of engine slot `dev` (cudaMemGetInfo only; cheap) */
+int bx_mem_info(int dev, uint64_t* free_bytes, uint64_t* total_bytes);
 /* Create per-device engines: streams, event pool, singular flag, arena of arena_bytes[i]
  * (0 = keep current), enable peer access between all pairs.  Idempotent; re-init with a
  * larger arena grows the reservation. */

@@ -35,6 +35,7 @@ _SIGS = {
     "bx_version": [],
     "bx_device_count": [_pi],
     "bx_device_info": [_i, C.c_char_p, _i, _pi, _pu64, _pu64],
+    "bx_mem_info": [_i, _pu64, _pu64],
     "bx_init": [_i, _pi, _pu64, _i],
     "bx_shutdown": [],
     "bx_arena_base": [_i, _pu64],

@@ -382,6 +382,17 @@ int bx_device_info(int dev, char* name, int name_len, int* sms, uint64_t* total_
   return BX_OK;
 }
 
+int bx_mem_info(int dev, uint64_t* free_bytes, uint64_t* total_bytes) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+  *free_bytes = fr;
+  *total_bytes = tot;
+  return BX_OK;
+}
+
 int bx_init(int ndev, const int* device_ids, const uint64_t* arena_bytes, int n_compute) {
   if (ndev <= 0 || n_compute <= 0 || n_compute > kMaxCompute) return set_err(BX_EINVAL, "bx_init: bad ndev/n_compute");
   int count = 0;

@@ -130,6 +130,8 @@ class Metrics:
     host_fetches: int = 0
     devices: dict = field(default_factory=dict)
     total_flops: int = 0
+    wall_seconds: float = 0.0
+    phases: dict = field(default_factory=dict)
 
     def to_dict(self) -> dict:
         return {

@@ -53,6 +53,11 @@ class CudaEngine:
         return dict(name=name.value.decode(), sms=sms.value, total_bytes=tot.value,
                     free_bytes=free.value)
 
+    def free_bytes(self, slot: int) -> int:
+        free, tot = C.c_uint64(), C.c_uint64()
+        N.check(self.lib.bx_mem_info(slot, C.byref(free), C.byref(tot)), "mem info")
+        return free.value
+
     def ensure_arenas(self, capacities: dict) -> None:
         """Grow-only per-device reservations (one cudaMalloc each); {slot: bytes}."""
         need = [max(int(capacities.get(i, 0)), cur) for i, cur in enumerate(self._arena)]

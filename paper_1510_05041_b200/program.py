@@ -52,9 +52,12 @@ def scratch_key(i: int) -> tuple:
     return ("#scratch", i)
 
 
-def compile_task(task: Task, call, chunk_steps: int) -> Program:
+def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0) -> Program:
+    """``first_chunk`` (if > 0) caps the task's first GEMM launch so its kernel can start
+    as soon as the first few input tiles have landed (pipeline ramp-up)."""
+    ckey = (chunk_steps, first_chunk)
     cache = getattr(task, "_bx_prog", None)
-    if cache is not None and cache[0] == chunk_steps:
+    if cache is not None and cache[0] == ckey:
         return cache[1]
     h, w = task.out_ref.phys_height, task.out_ref.phys_width
     tri = 1 if call.uplo == "lower" else 2
@@ -72,8 +75,11 @@ def compile_task(task: Task, call, chunk_steps: int) -> Program:
 
     def add(ta, tb, tr, alpha, beta, a, b, d, k):
         nonlocal cur
+        cap = chunk_steps
+        if first_chunk and not any(type(o) is GemmOp for o in ops):
+            cap = min(first_chunk, chunk_steps)
         if (cur is None or (cur[0], cur[1], cur[2], cur[3]) != (ta, tb, tr, alpha)
-                or beta != 1.0 or len(cur[5]) >= chunk_steps):
+                or beta != 1.0 or len(cur[5]) >= cap):
             flush()
             cur = [ta, tb, tr, alpha, beta, [], k]
         cur[5].append((a, b, d))
@@ -110,5 +116,5 @@ def compile_task(task: Task, call, chunk_steps: int) -> Program:
             raise ValueError(f"unknown step kind {kind!r}")
     flush()
     prog = Program(tuple(ops), tuple(scratch))
-    task._bx_prog = (chunk_steps, prog)
+    task._bx_prog = (ckey, prog)
     return prog

@@ -112,6 +112,7 @@ class TaskPlan:
     matrices: dict
     total_flops: int = 0
     dtype: np.dtype = field(default_factory=lambda: np.dtype(np.float64))
+    snapshot_alias: Optional[str] = None   # TRMM snapshot id when it aliases live storage
 
     def initially_ready(self) -> list:
         return [t for t in self.tasks if t.deps_remaining == 0]
@@ -365,27 +366,38 @@ def _structure_key(call: RoutineCall) -> tuple:
             str(call.c.matrix.storage.dtype))
 
 
-def generate_tasks(call: RoutineCall, cache: bool = True) -> TaskPlan:
+def generate_tasks(call: RoutineCall, cache: bool = True, snapshot: str = "copy") -> TaskPlan:
     """Expand a call into its task plan (reference routines.py:383-441).
 
     The task structure is a pure function of shapes / flags / scalars, so it is memoised
     (``cache``): a repeated call of the same shape rebinds the cached tasks to the new
-    operand storage instead of re-planning."""
+    operand storage instead of re-planning.
+
+    TRMM reads a snapshot of its in-place operand.  ``snapshot="copy"`` takes a host copy
+    (the reference, routines.py:393-400); ``"alias"`` lets the snapshot descriptor share
+    the live storage — valid only for an executor that fetches every snapshot tile before
+    the task owning that tile writes it back and never re-fetches it afterwards (the GPU
+    runtime pins snapshot tiles on device for the whole call, see scheduler.py)."""
     validate(call)
     t = call.c.tile_size
     matrices = {tm.matrix_id: tm.matrix for tm in (call.a, call.c, call.b) if tm is not None}
     snap = None
     if call.kind == "trmm":
         src = call.c.matrix
+        if snapshot not in ("copy", "alias"):
+            raise InvalidArgumentError(f"bad snapshot mode {snapshot!r}")
         sd = MatrixDesc(src.matrix_id + ".snapshot", src.rows, src.cols, src.leading_dim,
-                        src.storage.copy(), src.base_offset)
+                        src.storage.copy() if snapshot == "copy" else src.storage,
+                        src.base_offset)
         snap = TiledMatrix(sd, t, call.c.tile_rows, call.c.tile_cols)
         matrices[sd.matrix_id] = sd
     skey = _structure_key(call) if cache else None
     hit = _PLAN_CACHE.get(skey) if cache else None
     if hit is not None:
         tasks, total = hit
-        return TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
+        plan = TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
+        plan.snapshot_alias = snap.matrix_id if (snap is not None and snapshot == "alias") else None
+        return plan
     planner = _PLANNERS[call.kind]
     memo = {}
 
@@ -425,7 +437,9 @@ def generate_tasks(call: RoutineCall, cache: bool = True) -> TaskPlan:
         if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
         _PLAN_CACHE[skey] = (tasks, total)
-    return TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
+    plan = TaskPlan(call, t, tasks, matrices, total, call.c.matrix.storage.dtype)
+    plan.snapshot_alias = snap.matrix_id if (snap is not None and snapshot == "alias") else None
+    return plan
 
 
 def gemm_flop_fraction(plan: TaskPlan) -> float:

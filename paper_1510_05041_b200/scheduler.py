@@ -78,6 +78,7 @@ class RunOptions:
     n_streams: int = 4
     chunk_steps: int = 16              # k-steps fused per kernel launch
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
+    first_chunk_steps: int = 4         # shorter first launch per task (ramp-up); 0 = off
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -244,6 +245,8 @@ class _GpuWorker:
         self.tile = runtime.plan.tile_size
         self.trace_on = opts.record_trace
         self.epoch = None
+        self._snap_id = runtime.plan.snapshot_alias
+        self._permanent = []
         grp = runtime.topology.peer_group_of(desc)
         self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
                                       if d.device_id != desc.device_id
@@ -403,6 +406,11 @@ class _GpuWorker:
                         self.host_fetches += 1
                     self.l1_hits += mult - 1
                 cache.pin(blk)
+                if key[0] == self._snap_id:
+                    # aliased TRMM snapshot tile: keep it resident for the whole call so
+                    # nobody re-fetches it from host after its owner wrote it back
+                    cache.pin(blk)
+                    self._permanent.append(blk)
             act.pins.append((cache, blk))
             wait = None
             if blk.ready_ev is not None and not blk.ready_done:
@@ -467,7 +475,7 @@ class _GpuWorker:
                 act.events.append(ev)
                 act.pending_waits.append(ev)
                 self.dm.h2d_bytes += h * w * self.esz
-            prog = compile_task(task, call, opts.chunk_steps)
+            prog = compile_task(task, call, opts.chunk_steps, opts.first_chunk_steps)
             if opts.l1_enabled:
                 res = self._resolve_task(task)
             else:
@@ -565,6 +573,9 @@ class _GpuWorker:
         return all(a is None for a in self.active)
 
     def release_all(self) -> None:
+        if self._permanent:
+            self.cache.release(self._permanent)
+            self._permanent = []
         for blk in self.cache.blocks():
             self._on_evict(blk)
 
@@ -584,7 +595,7 @@ def task_keys(task: Task) -> dict:
     return keys
 
 
-def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: int) -> int:
+def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[int]) -> int:
     """Enough for every tile of every input matrix plus the in-flight C / scratch buffers,
     capped at 90 % of free HBM (no eviction at BASELINE sizes on a 180 GB B200)."""
     esz = plan.dtype.itemsize
@@ -600,14 +611,17 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: int) -> i
         want += -(-per_col_tile * t * col_tiles * esz // 256) * 256 + 256 * col_tiles * (rows_full + 1)
     per_tile = device_ld(t) * t * esz
     want += (options.n_streams * options.tasks_per_stream + 2) * 2 * per_tile + (64 << 20)
+    if free_bytes is None:
+        return want
     cap = int(free_bytes * 0.9) - (1 << 30)
     return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
 
 
 def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
-             options: Optional[RunOptions] = None, engine=None) -> RunResult:
+             options: Optional[RunOptions] = None, engine=None, _t_plan: float = 0.0) -> RunResult:
     """Execute a task plan on the topology's GPUs; the host output holds the result."""
     from .engine import get_engine
+    t_setup0 = time.perf_counter()
     options = options or RunOptions()
     if options.execution not in ("deterministic", "concurrent"):
         raise ConfigError(f"unknown execution mode {options.execution!r}")
@@ -628,14 +642,29 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         slot = engine.slot(d.device_id)
         want = d.arena_capacity or options.arena_bytes
         if not want:
-            want = _auto_arena_bytes(plan, options, engine.device_info(slot)["free_bytes"]
-                                     + engine.arena_capacity(slot))
+            want = _auto_arena_bytes(plan, options, None)
+            if want > engine.arena_capacity(slot):     # only then ask the driver (slow query)
+                want = _auto_arena_bytes(plan, options, engine.free_bytes(slot)
+                                         + engine.arena_capacity(slot))
         if want <= WORKING_SET_TILES * per_tile:
             raise ConfigError(
                 f"device {d.device_id}: arena of {want} bytes cannot hold the "
                 f"{WORKING_SET_TILES}-tile working set at tile size {plan.tile_size}")
         caps[slot] = want
     engine.ensure_arenas(caps)
+    if plan.snapshot_alias is not None:
+        snap = plan.matrices[plan.snapshot_alias]
+        snap_bytes = (-(-snap.rows // plan.tile_size) * device_ld(plan.tile_size)
+                      * snap.cols * esz)
+        if (options.execution != "deterministic"
+                or any(snap_bytes + 2 * WORKING_SET_TILES * per_tile > c for c in caps.values())):
+            # cannot keep every snapshot tile resident (or per-GPU threads could race a host
+            # fetch against a write-back): take the reference's host copy
+            from .tiling import MatrixDesc as _MD
+            plan.matrices[plan.snapshot_alias] = _MD(
+                snap.matrix_id, snap.rows, snap.cols, snap.leading_dim, snap.storage.copy(),
+                snap.base_offset)
+            plan.snapshot_alias = None
     # Page-lock the operands for the DMA engine.  Buffers pinned by the caller beforehand
     # (``pin_host``; the paper excludes page-locking from timing) stay
     # pinned; the ones pinned here are unpinned when the call returns.
@@ -653,6 +682,7 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     for w in workers:
         w.epoch = engine.record(w.slot, 0, timing=True)
     t0 = time.perf_counter()
+    t_setup = t0 - t_setup0
     try:
         if options.execution == "deterministic":
             _drive_single(rt, workers)
@@ -667,10 +697,13 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         _unpin(engine, pinned_here)
         raise
     wall = time.perf_counter() - t0
+    t_fin0 = time.perf_counter()
     metrics = _finalize(rt, workers, wall)
     for w in workers:
         w.release_all()
     _unpin(engine, pinned_here)
+    metrics.phases = {"plan_s": _t_plan, "setup_s": t_setup, "drive_s": wall,
+                      "finalize_s": time.perf_counter() - t_fin0}
     return RunResult(metrics, sorted(rt.trace, key=lambda e: (e.time_start, e.device, e.time_end)),
                      {w.device_id: w.tasks_done for w in workers}, plan)
 
@@ -767,4 +800,6 @@ def _finalize(rt: _Runtime, workers, wall: float) -> Metrics:
 def run_call(call: RoutineCall, topology: Optional[Topology] = None,
              options: Optional[RunOptions] = None, engine=None) -> RunResult:
     """Plan and execute one routine call; on return the host output holds the result."""
-    return run_plan(generate_tasks(call), topology, options, engine)
+    t0 = time.perf_counter()
+    plan = generate_tasks(call, snapshot="alias")
+    return run_plan(plan, topology, options, engine, _t_plan=time.perf_counter() - t0)

@@ -61,6 +61,9 @@ class FakeEngine:
     def device_info(self, slot):
         return dict(name="fake", sms=148, total_bytes=1 << 34, free_bytes=self.default_arena)
 
+    def free_bytes(self, slot):
+        return self.default_arena
+
     def ensure_arenas(self, caps):
         for slot, c in caps.items():
             if c > self._arena_cap[slot]:

@@ -23,6 +23,7 @@ class NullEngine:
 
     def slot(self, d): return d
     def device_info(self, s): return dict(free_bytes=170 << 30)
+    def free_bytes(self, s): return 170 << 30
     def ensure_arenas(self, caps):
         for k, v in caps.items():
             self.cap[k] = max(self.cap[k], v)

@@ -12,14 +12,13 @@ from paper_1510_05041_b200.engine import get_engine
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 t = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-tps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+tps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+fc = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 call = build_call("gemm", m=n, n=n, k=n, tile_size=t, seed=0, alpha=1.0, beta=1.0)
 eng = get_engine([0])
 for x in (call.a, call.b, call.c):
     eng.register_host(x.matrix.storage)
-kw = dict(chunk_steps=chunk)
-if tps != 1:
-    kw["tasks_per_stream"] = tps
+kw = dict(chunk_steps=chunk, tasks_per_stream=tps, first_chunk_steps=fc)
 run_call(call, options=RunOptions(**kw))
 t0 = time.perf_counter()
 res = run_call(call, options=RunOptions(**kw))
@@ -27,6 +26,7 @@ wall = time.perf_counter() - t0
 res2 = run_call(call, options=RunOptions(record_trace=True, **kw))
 tr = res2.trace
 m = res.metrics
+print("phases", {k: round(v * 1e3, 2) for k, v in res.metrics.phases.items()})
 print(f"untraced: wall {wall*1e3:.1f} ms makespan {m.makespan_seconds*1e3:.1f} ms "
       f"-> {res.plan.total_flops / m.makespan_seconds / 1e12:.2f} TF/s")
 print(f"traced makespan {res2.metrics.makespan_seconds*1e3:.1f} ms")
