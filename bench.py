@@ -325,6 +325,8 @@ def main():
     lib = NN.load()
     NN.require_gpu()
     eng = get_engine(list(range(args.gpus)), 4)
+    if os.environ.get("BX_TRSM_LEAF"):
+        NN.check(lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"])), "trsm leaf")
     peak = C.c_double()
     NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
     if dist:

@@ -115,6 +115,9 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
                     uint64_t a, int lda, uint64_t b, int ldb, double beta, uint64_t c, int ldc);
 /* tuning knob: tile configuration of the FP64 task GEMM (0 default; 1, 2 alternates) */
 int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 deep, 3 slack-2 */
+/* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 128); larger
+ * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
+int bx_set_trsm_leaf(int n);
 /* register-only DMMA loop: measured FP64 tensor peak for the roofline denominator */
 int bx_fp64_peak_probe(int dev, int iters, double* tflops);
 

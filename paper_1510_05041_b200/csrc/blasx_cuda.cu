@@ -146,6 +146,7 @@ bool need_attr(unsigned bit) {
 }
 
 int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
+int g_trsm_leaf = 128;   // triangle order solved by a leaf kernel; larger ones recurse
 
 template <class Cfg, bool TA, bool TB>
 int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
@@ -252,6 +253,13 @@ int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int
   t.rev = right ? !eff_upper : eff_upper;
   t.right = right; t.unit = unit; t.alpha = alpha; t.flag = flag;
   if (t.n == 0 || t.nrhs == 0) return BX_OK;
+  if (t.n <= bx::LEAF_N) {
+    int per_cta = bx::LEAF_RHS * bx::LEAF_WARPS;
+    bx::trsm_leaf_kernel<<<(t.nrhs + per_cta - 1) / per_cta, bx::LEAF_WARPS * 32, 0, s>>>(t);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    return BX_OK;
+  }
   size_t smem = (size_t)t.n * bx::T_YP * sizeof(double);
   if (need_attr(1u << 8)) {
     CUDA_TRY(cudaFuncSetAttribute(bx::trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -275,7 +283,9 @@ int trsm_rec(cudaStream_t s, int right, int eff_upper, int trans, int unit, int 
     if (rc) return rc;
     alpha = 1.0;
   }
-  int n1 = ((n / 2) + 31) / 32 * 32, n2 = n - n1;
+  // split on a multiple of the leaf order so every leaf is full except the last
+  int n1 = ((n / 2) + leaf_max - 1) / leaf_max * leaf_max, n2 = n - n1;
+  if (n1 >= n) n1 = n - leaf_max;
   // E block (r0, c0, rows, cols) -> A pointer + transpose flag
   auto eblk = [&](int r0, int c0) -> const double* {
     return trans ? a + (size_t)r0 * lda + c0 : a + (size_t)c0 * lda + r0;
@@ -585,7 +595,7 @@ int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int 
   if (rc) return rc;
   int eff_upper = (upper != 0) != (trans != 0);
   rc = trsm_rec(s, side_right, eff_upper, trans, unit, h, w, alpha, (const double*)(D->arena + a_off), lda,
-                (double*)(D->arena + b_off), ldb, D->flag_dev, 1024);
+                (double*)(D->arena + b_off), ldb, D->flag_dev, g_trsm_leaf);
   if (rc) return rc;
   return finish(dev, s, ev_out);
 }
@@ -767,6 +777,12 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
 
 int bx_set_gemm_variant(int v) {
   g_gemm_variant = v;
+  return BX_OK;
+}
+
+int bx_set_trsm_leaf(int n) {
+  if (n < 32 || n > bx::T_NMAX) return set_err(BX_EINVAL, "trsm leaf must be in [32, 2048]");
+  g_trsm_leaf = n;
   return BX_OK;
 }
 

@@ -58,23 +58,32 @@ __global__ void __launch_bounds__(T_THREADS) trsm_panel_kernel(const __grid_cons
   const int g = lane >> 2, q = lane & 3;
   for (int i0 = 0; i0 < n; i0 += T_BLK) {
     const int nb = min(T_BLK, n - i0);
-    for (int idx = tid; idx < T_BLK * T_BLK; idx += T_THREADS) {
-      int j = idx / T_BLK, r = idx % T_BLK;
-      double v = 0.0;
-      if (r < nb && j < nb && r >= j && !(t.unit && r == j)) v = trsm_L(t, i0 + r, i0 + j);
-      ls[j * (T_BLK + 1) + r] = v;
+    {
+      double v[T_BLK * T_BLK / T_THREADS];
+#pragma unroll
+      for (int q = 0; q < T_BLK * T_BLK / T_THREADS; ++q) {
+        const int idx = tid + q * T_THREADS, j = idx / T_BLK, r = idx % T_BLK;
+        v[q] = (r < nb && j < nb && r >= j && !(t.unit && r == j)) ? trsm_L(t, i0 + r, i0 + j) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < T_BLK * T_BLK / T_THREADS; ++q) {
+        const int idx = tid + q * T_THREADS;
+        ls[(idx / T_BLK) * (T_BLK + 1) + idx % T_BLK] = v[q];
+      }
     }
     __syncthreads();
     {
       // substitution on the diagonal block: warp -> RHS, lane -> row
       const int r = lane;
       double y = (r < nb) ? ys[(i0 + r) * T_YP + warp] : 0.0;
+      double inv = 1.0;
+      if (!t.unit && r < nb) {
+        const double dd = ls[r * (T_BLK + 1) + r];
+        if (dd == 0.0) atomicOr(t.flag, 1);
+        inv = 1.0 / dd;
+      }
       for (int j = 0; j < nb; ++j) {
-        if (r == j && !t.unit) {
-          double dd = ls[j * (T_BLK + 1) + j];
-          if (dd == 0.0) atomicOr(t.flag, 1);
-          y = y / dd;
-        }
+        if (r == j && !t.unit) y *= inv;
         double x = __shfl_sync(0xffffffffu, y, j);
         if (r > j) y = y - ls[j * (T_BLK + 1) + r] * x;
       }
@@ -140,6 +149,102 @@ __global__ void scale_kernel(double* __restrict__ b, int ld, int h, int w, doubl
   int r = blockIdx.x * 32 + threadIdx.x;
   int c = blockIdx.y * 8 + threadIdx.y;
   if (r < h && c < w) b[(size_t)c * ld + r] *= alpha;
+}
+
+// ---------------------------------------------------------------------------------------
+// Leaf solve for triangle order n <= 64 with many right-hand sides per warp.
+// Lane r of a warp owns logical rows r and r + 32 for LEAF_RHS right-hand sides held in
+// registers; the diagonal is walked column by column (right-looking substitution):
+// the owner lane divides its LEAF_RHS values by L(j,j) (independent divisions -> ILP),
+// the solved row is broadcast with shuffles and every lane below updates its rows with
+// one FMA per right-hand side.  Warps are independent (no CTA barrier after staging L),
+// so per-SM throughput scales with LEAF_RHS instead of being bound by the serial
+// division/shuffle latency of one right-hand side.
+// ---------------------------------------------------------------------------------------
+constexpr int LEAF_RHS = 16, LEAF_WARPS = 8, LEAF_N = 64;
+
+__global__ void __launch_bounds__(LEAF_WARPS * 32) trsm_leaf_kernel(const __grid_constant__ TrsmArgs t) {
+  __shared__ double ls[LEAF_N * (LEAF_N + 1)];   // ls[j*65 + r] = L(r, j)
+  const int n = t.n;
+  {
+    // all loads in flight before the first store (one round trip, not n*n/256)
+    constexpr int PER = LEAF_N * LEAF_N / (LEAF_WARPS * 32);
+    double v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int idx = threadIdx.x + q * LEAF_WARPS * 32;
+      const int j = idx / LEAF_N, r = idx % LEAF_N;
+      v[q] = (r < n && j < n && r >= j && !(t.unit && r == j)) ? trsm_L(t, r, j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int idx = threadIdx.x + q * LEAF_WARPS * 32;
+      ls[(idx / LEAF_N) * (LEAF_N + 1) + idx % LEAF_N] = v[q];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col0 = (blockIdx.x * LEAF_WARPS + warp) * LEAF_RHS;
+  if (col0 >= t.nrhs) return;
+  const int r0 = lane, r1 = lane + 32;
+  double y0[LEAF_RHS], y1[LEAF_RHS];
+#pragma unroll
+  for (int c = 0; c < LEAF_RHS; ++c) {
+    const int col = col0 + c;
+    const bool cv = col < t.nrhs;
+    y0[c] = (cv && r0 < n) ? t.alpha * *trsm_Y(t, r0, col) : 0.0;
+    y1[c] = (cv && r1 < n) ? t.alpha * *trsm_Y(t, r1, col) : 0.0;
+  }
+  // reciprocals of the diagonal, computed once per lane off the critical path (a division
+  // per solved row per RHS on one lane serialises the whole warp)
+  double inv0 = 1.0, inv1 = 1.0;
+  if (!t.unit) {
+    if (r0 < n) {
+      const double d = ls[r0 * (LEAF_N + 1) + r0];
+      if (d == 0.0) atomicOr(t.flag, 1);
+      inv0 = 1.0 / d;
+    }
+    if (r1 < n) {
+      const double d = ls[r1 * (LEAF_N + 1) + r1];
+      if (d == 0.0) atomicOr(t.flag, 1);
+      inv1 = 1.0 / d;
+    }
+  }
+  // Branch-free column sweep: the owner lane scales its row by 1/L(j,j) (other lanes
+  // multiply by 1), broadcasts it, and every lane subtracts L(r,j) x_j (0 above the
+  // diagonal).  Rows 0..31 and 32..63 are separate sweeps so no per-element selects remain.
+  const bool nonunit = !t.unit;
+  for (int j = 0; j < n && j < 32; ++j) {
+    const double sc = (nonunit && lane == j) ? inv0 : 1.0;
+    const double l0 = (lane > j) ? ls[j * (LEAF_N + 1) + r0] : 0.0;
+    const double l1 = (r1 < n) ? ls[j * (LEAF_N + 1) + r1] : 0.0;
+#pragma unroll
+    for (int c = 0; c < LEAF_RHS; ++c) {
+      y0[c] *= sc;
+      const double x = __shfl_sync(0xffffffffu, y0[c], j);
+      y0[c] = fma(-l0, x, y0[c]);
+      y1[c] = fma(-l1, x, y1[c]);
+    }
+  }
+  for (int j = 32; j < n; ++j) {
+    const int owner = j - 32;
+    const double sc = (nonunit && lane == owner) ? inv1 : 1.0;
+    const double l1 = (lane > owner && r1 < n) ? ls[j * (LEAF_N + 1) + r1] : 0.0;
+#pragma unroll
+    for (int c = 0; c < LEAF_RHS; ++c) {
+      y1[c] *= sc;
+      const double x = __shfl_sync(0xffffffffu, y1[c], owner);
+      y1[c] = fma(-l1, x, y1[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < LEAF_RHS; ++c) {
+    const int col = col0 + c;
+    if (col < t.nrhs) {
+      if (r0 < n) *trsm_Y(t, r0, col) = y0[c];
+      if (r1 < n) *trsm_Y(t, r1, col) = y1[c];
+    }
+  }
 }
 
 }  // namespace bx

@@ -35,7 +35,7 @@ from typing import Optional
 
 import numpy as np
 
-from .cache import HOST_FETCH, L1_HIT, L2_HIT, CoherenceDirectory, DeviceTileCache
+from .cache import HOST_FETCH, L1_HIT, L2_HIT, CoherenceDirectory, DeviceTileCache, LruBlock
 from .devices import (DeviceMetrics, Metrics, Topology, TraceEvent, discover_topology,
                       exposed_comm_time)
 from .errors import CapacityDeadlockError, ConfigError, SingularMatrixError
@@ -79,6 +79,7 @@ class RunOptions:
     chunk_steps: int = 16              # k-steps fused per kernel launch
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
     first_chunk_steps: int = 4         # shorter first launch per task (ramp-up); 0 = off
+    retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -247,6 +248,7 @@ class _GpuWorker:
         self.epoch = None
         self._snap_id = runtime.plan.snapshot_alias
         self._permanent = []
+        self._retain = opts.retain_outputs and runtime.plan.call.kind == "trsm"
         grp = runtime.topology.peer_group_of(desc)
         self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
                                       if d.device_id != desc.device_id
@@ -543,12 +545,23 @@ class _GpuWorker:
         for cache, blk in act.pins + act.launched_pins:
             cache.unpin(blk)
         act.pins = act.launched_pins = []
-        self.arena.free(act.c_off)
         for off in act.scratch:
             self.arena.free(off)
         for ev in act.events:
             self.eng.release(ev)
-        self.runtime.directory.note_write_back(task.out_ref.key())
+        key = task.out_ref.key()
+        self.runtime.directory.note_write_back(key)
+        if self._retain and self.runtime.options.l1_enabled and not self.cache.contains(key):
+            # write-back-then-retain: after the D2H the device copy equals
+            # the host copy, so the tile moves M -> E instead of M -> I and dependents read
+            # it from L1 / over NVLink instead of re-fetching it from the host
+            out = task.out_ref
+            blk = LruBlock(key, act.c_off, act.c_ld * out.phys_width * self.esz, act.c_ld,
+                           self.device_id)
+            blk.ready_done = True
+            self.cache.insert_front(blk)
+        else:
+            self.arena.free(act.c_off)
         if self.plan.call.kind == "trsm" and self.eng.singular(self.slot, reset=True):
             raise SingularMatrixError("zero on a non-unit triangular diagonal")
         self.tasks_done += 1

@@ -180,3 +180,79 @@ for var in (variants if "--perf" in sys.argv else []):
             print(f"   trans {tt}: {ms.value:.3f} ms {2*n**3/ms.value/1e9:.2f} TF/s")
         for p in ptrs:
             lib.bx_dev_free(0, p)
+
+if "--trsm-perf" in sys.argv:
+    for leaf in (32, 64, 128):
+        lib.bx_set_trsm_leaf(leaf)
+        print("leaf", leaf)
+        for n, other in [(1024, 1024), (2048, 2048)]:
+            for side in ("left", "right"):
+                _next[0] = 0
+                a = (rng.random((n, n)) * 2 - 1) / n
+                np.fill_diagonal(a, 1.5)
+                b = rng.random((n, other) if side == "left" else (other, n)) * 2 - 1
+                oa, la = put(a)
+                ob, lb = put(b)
+                e0, e1, ev = C.c_int(), C.c_int(), C.c_int()
+                args = (0, 0, side == "right", 0, 0, 0, b.shape[0], b.shape[1], 1.0, oa, la, ob, lb, 0, None, C.byref(ev))
+                N.check(lib.bx_trsm_tile(*args))
+                lib.bx_event_sync(ev.value)
+                best = 1e9
+                for _ in range(3):
+                    lib.bx_event_record(0, 0, 1, C.byref(e0))
+                    N.check(lib.bx_trsm_tile(*args))
+                    lib.bx_event_record(0, 0, 1, C.byref(e1))
+                    lib.bx_event_sync(e1.value)
+                    ms = C.c_float()
+                    lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
+                    best = min(best, ms.value)
+                fl = n * n * other
+                print(f"trsm {side} n={n} rhs={other}: {best*1e3:.1f} us  {fl/best/1e9:.2f} TF/s")
+
+if "--small-gemm" in sys.argv:
+    for var in variants:
+        lib.bx_set_gemm_variant(var)
+        for (m, n, k) in [(64, 1024, 64), (128, 1024, 128), (512, 1024, 512), (1024, 1024, 1024), (64, 64, 64)]:
+            ptrs = []
+            for nel in (m * k, k * n, m * n):
+                p = C.c_uint64()
+                N.check(lib.bx_dev_alloc(0, nel * 8, C.byref(p)))
+                N.check(lib.bx_dev_fill_uniform(0, p.value, nel, 3, 0))
+                ptrs.append(p.value)
+            e0, e1 = C.c_int(), C.c_int()
+            N.check(lib.bx_dgemm_device(0, 0, 0, 0, m, n, k, 1.0, ptrs[0], m, ptrs[1], k, 1.0, ptrs[2], m))
+            lib.bx_device_sync(0)
+            lib.bx_event_record(0, 0, 1, C.byref(e0))
+            for _ in range(20):
+                N.check(lib.bx_dgemm_device(0, 0, 0, 0, m, n, k, 1.0, ptrs[0], m, ptrs[1], k, 1.0, ptrs[2], m))
+            lib.bx_event_record(0, 0, 1, C.byref(e1))
+            lib.bx_event_sync(e1.value)
+            ms = C.c_float()
+            lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
+            print(f"variant {var} gemm {m}x{n}x{k}: {ms.value / 20 * 1e3:.1f} us per launch")
+            for p in ptrs:
+                lib.bx_dev_free(0, p)
+
+if "--launch-overhead" in sys.argv:
+    import time as _t
+    p = C.c_uint64()
+    N.check(lib.bx_dev_alloc(0, 1 << 20, C.byref(p)))
+    ptrs = []
+    for nel in (64 * 64, 64 * 64, 64 * 64):
+        q = C.c_uint64()
+        N.check(lib.bx_dev_alloc(0, nel * 8, C.byref(q)))
+        ptrs.append(q.value)
+    e0, e1 = C.c_int(), C.c_int()
+    for label, fn in [("fill n=1", lambda: lib.bx_dev_fill_uniform(0, p.value, 1, 1, 0)),
+                      ("gemm 64^3", lambda: lib.bx_dgemm_device(0, 0, 0, 0, 64, 64, 64, 1.0, ptrs[0], 64, ptrs[1], 64, 1.0, ptrs[2], 64))]:
+        fn(); lib.bx_device_sync(0)
+        t0 = _t.perf_counter()
+        lib.bx_event_record(0, 0, 1, C.byref(e0))
+        for _ in range(50):
+            fn()
+        lib.bx_event_record(0, 0, 1, C.byref(e1))
+        t1 = _t.perf_counter()
+        lib.bx_event_sync(e1.value)
+        ms = C.c_float()
+        lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
+        print(f"{label}: host {(t1 - t0) / 50 * 1e6:.1f} us/call, gpu {ms.value / 50 * 1e3:.1f} us/launch")
