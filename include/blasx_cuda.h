@@ -83,6 +83,12 @@ int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int
                  const uint64_t* a_off, const int* lda, const uint64_t* b_off, const int* ldb,
                  const int* depth, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
                  const int* wait, int* ev_out);
+/* fp32 task GEMM (SGEMM) on tcgen05.mma.kind::tf32 with TMEM accumulators and TMA operand
+ * staging; same operands/semantics as bx_gemm_task (no triangle mode). Leading dimensions
+ * must be multiples of 4 elements and operands 16-byte aligned. */
+int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps, const uint64_t* a_off,
+                  const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, float alpha,
+                  float beta, uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out);
 /* in-place triangular solve of B (h x w) against the diagonal tile A */
 int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h,
                  int w, double alpha, uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait,
@@ -118,6 +124,8 @@ int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 d
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 128); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);
+int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha,
+                    uint64_t a, int lda, uint64_t b, int ldb, float beta, uint64_t c, int ldc);
 /* register-only DMMA loop: measured FP64 tensor peak for the roofline denominator */
 int bx_fp64_peak_probe(int dev, int iters, double* tflops);
 

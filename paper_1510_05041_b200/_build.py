@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libblasx_cuda.so")
 SOURCES = ["blasx_cuda.cu"]
-DEPS = ["bx_gemm_dmma.cuh", "bx_trsm.cuh"]
+DEPS = ["bx_gemm_dmma.cuh", "bx_trsm.cuh", "bx_sgemm_tc.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

@@ -15,7 +15,10 @@
 #include <vector>
 
 #include "../../include/blasx_cuda.h"
+#include <unordered_map>
+
 #include "bx_gemm_dmma.cuh"
+#include "bx_sgemm_tc.cuh"
 #include "bx_trsm.cuh"
 
 namespace {
@@ -195,6 +198,105 @@ int launch_gemm(int ta, int tb, const bx::GemmTask& t, cudaStream_t s) {
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// ---- TMA tensor maps (driver entry point fetched at run time: no -lcuda) --------------
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled g_encode = nullptr;
+
+struct MapKey {
+  uint64_t ptr, rows, cols, ld;
+  uint32_t box0, box1, swz;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box0 == o.box0 && box1 == o.box1 &&
+           swz == o.swz;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<uint64_t>()(k.ptr ^ (k.rows * 0x9E3779B97F4A7C15ull) ^ (k.cols << 20) ^ (k.ld << 40) ^
+                                 ((uint64_t)k.box0 << 8) ^ ((uint64_t)k.box1 << 16) ^ ((uint64_t)k.swz << 4));
+  }
+};
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2-d fp32 column-major matrix (rows contiguous, leading dimension ld elements) -> tensor
+// map with a {box0 (rows), box1 (cols)} box, 128-B swizzle, zero fill out of bounds.
+int tensor_map_f32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0, uint32_t box1,
+                   CUtensorMapSwizzle swz, CUtensorMap* out) {
+  MapKey key{(uint64_t)base, rows, cols, ld, box0, box1, (uint32_t)swz};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) { *out = it->second; return BX_OK; }
+  }
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return set_err(BX_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (PFN_encodeTiled)fn;
+  }
+  cuuint64_t dims[2] = {rows, cols};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(BX_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_maps.size() > 65536) g_maps.clear();
+  g_maps[key] = m;
+  *out = m;
+  return BX_OK;
+}
+
+// fp32 task GEMM on tcgen05 (TF32 inputs, fp32 accumulation in TMEM)
+int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
+              const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c, int ldc) {
+  if (h <= 0 || w <= 0) return BX_OK;
+  if (ldc < h) return set_err(BX_EINVAL, "sgemm: ldc < h");
+  for (int s0 = 0; s0 < (nsteps > 0 ? nsteps : 1); s0 += bx::S_MAX_STEPS) {
+    bx::SgemmTask t;
+    memset(&t, 0, sizeof(t));
+    int n = nsteps - s0 < bx::S_MAX_STEPS ? nsteps - s0 : bx::S_MAX_STEPS;
+    if (n < 0) n = 0;
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.nsteps = n; t.ta = ta; t.tb = tb;
+    t.alpha = alpha;
+    t.beta = (s0 == 0) ? beta : 1.0f;
+    t.mn_lbo = 4096;   // MN-major: 32-wide MN groups (one TMA box) 4 KB apart
+    t.mn_sbo = 512;    //           4-row k groups of the 128B_BASE32B atom
+    for (int i = 0; i < n; ++i) {
+      const int j = s0 + i, d = depth[j];
+      if ((lda[j] & 3) || (ldb[j] & 3) || !aligned16(a[j]) || !aligned16(b[j]))
+        return set_err(BX_EINVAL, "sgemm: operands must be 16-byte aligned with leading dimensions multiple of 4");
+      t.steps[i].d = d;
+      int rc;
+      // A: untransposed M x K (MN-major boxes 32x32), transposed K x M (K-major box 32 x 128)
+      const CUtensorMapSwizzle MN = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, KM = CU_TENSOR_MAP_SWIZZLE_128B;
+      if (!ta) rc = tensor_map_f32(a[j], h, d, lda[j], 32, 32, MN, &t.steps[i].map_a);
+      else rc = tensor_map_f32(a[j], d, h, lda[j], bx::S_BK, bx::S_BM, KM, &t.steps[i].map_a);
+      if (rc) return rc;
+      // B: untransposed K x N (K-major box 32 x 256), transposed N x K (MN-major boxes 32x32)
+      if (!tb) rc = tensor_map_f32(b[j], d, w, ldb[j], bx::S_BK, bx::S_BN, KM, &t.steps[i].map_b);
+      else rc = tensor_map_f32(b[j], w, d, ldb[j], 32, 32, MN, &t.steps[i].map_b);
+      if (rc) return rc;
+    }
+    if (need_attr(1u << 9)) {
+      CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::S_SMEM_BYTES));
+    }
+    int tiles = ((h + bx::S_BM - 1) / bx::S_BM) * ((w + bx::S_BN - 1) / bx::S_BN);
+    bx::sgemm_tc_kernel<<<tiles, bx::S_THREADS, bx::S_SMEM_BYTES, s>>>(t);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+    if (nsteps <= 0) break;
+  }
+  return BX_OK;
+}
 
 // General gemm over raw pointers, splitting step lists longer than G_MAX_STEPS into
 // several launches (later launches accumulate with beta = 1).
@@ -580,6 +682,41 @@ int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int
   rc = gemm_raw(s, ta, tb, tri, h, w, nsteps, ap.data(), lda, bp.data(), ldb, depth, alpha, beta, (double*)(D->arena + c_off), ldc);
   if (rc) return rc;
   return finish(dev, s, ev_out);
+}
+
+int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps, const uint64_t* a_off,
+                  const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, float alpha, float beta,
+                  uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  if (nsteps < 0 || nsteps > 4096) return set_err(BX_EINVAL, "sgemm: bad step count");
+  std::vector<const float*> ap(nsteps > 0 ? nsteps : 1), bp(nsteps > 0 ? nsteps : 1);
+  for (int i = 0; i < nsteps; ++i) {
+    if (a_off[i] >= D->arena_bytes || b_off[i] >= D->arena_bytes) return set_err(BX_EINVAL, "sgemm: operand outside arena");
+    ap[i] = (const float*)(D->arena + a_off[i]);
+    bp[i] = (const float*)(D->arena + b_off[i]);
+  }
+  if (c_off + (uint64_t)ldc * w * 4 > D->arena_bytes) return set_err(BX_EINVAL, "sgemm: C outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  rc = sgemm_raw(s, ta, tb, h, w, nsteps, ap.data(), lda, bp.data(), ldb, depth, alpha, beta, (float*)(D->arena + c_off), ldc);
+  if (rc) return rc;
+  return finish(dev, s, ev_out);
+}
+
+int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha, uint64_t a, int lda,
+                    uint64_t b, int ldb, float beta, uint64_t c, int ldc) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  const float* ap = (const float*)a;
+  const float* bp = (const float*)b;
+  return sgemm_raw(s, ta, tb, m, n, 1, &ap, &lda, &bp, &ldb, &k, alpha, beta, (float*)c, ldc);
 }
 
 int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h, int w, double alpha,

@@ -1,0 +1,229 @@
+// SGEMM tile task on the 5th-generation tensor cores: tcgen05.mma.kind::tf32 with the
+// accumulator in TMEM, operands streamed into 128B-swizzled shared memory by TMA
+// (cp.async.bulk.tensor) under an mbarrier full/empty ring.
+//
+// Same task contract as the FP64 kernel (bx_gemm_dmma.cuh):
+//     C[h x w] = alpha * sum_s op_s(A_s) op_s(B_s) + beta * C      (fp32 storage)
+// The reference has no single-precision path (/root/reference/pkg/src/tileblas/tiling.py:
+// 57-60 rejects float32); this kernel serves the cfg5 SGEMM workload.  tcgen05 has no
+// fp32 kind: kind::tf32 rounds the inputs to 10-bit mantissas and accumulates in fp32.
+//
+// Warp roles (192 threads, 1 CTA per SM):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers, alpha/beta, coalesced stores
+// CTA tile BM=128 x BN=256, BK=32 fp32 (one 128-B swizzle row), 4 stages (192 KB).
+// Operand major-ness per step: A is MN-major when stored untransposed (column-major
+// M x K), K-major when transposed; B is K-major untransposed, MN-major transposed.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bx {
+
+constexpr int S_BM = 128, S_BN = 256, S_BK = 32, S_STAGES = 4, S_THREADS = 192;
+constexpr int S_MAX_STEPS = 16;
+constexpr int S_A_BYTES = S_BM * S_BK * 4;            // 16 KB
+constexpr int S_B_BYTES = S_BN * S_BK * 4;            // 32 KB
+constexpr int S_STAGE_BYTES = S_A_BYTES + S_B_BYTES;
+constexpr int S_SMEM_BYTES = S_STAGES * S_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int S_TMEM_COLS = 256;
+
+struct SgemmStep {
+  CUtensorMap map_a;   // 64-B aligned by declaration
+  CUtensorMap map_b;
+  int d;               // reduction extent of the step
+  int pad_[31];
+};
+
+struct SgemmTask {
+  SgemmStep steps[S_MAX_STEPS];
+  float* c;
+  int ldc, h, w, nsteps;
+  int ta, tb;          // operand stored transposed
+  float alpha, beta;
+  int mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void s_mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void s_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n}\n" ::"r"(s_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void s_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void s_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void s_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// shared-memory matrix descriptor (sm100 "version 1").  layout 2 = SWIZZLE_128B (K-major
+// operands, 8 rows x 128 B atoms); layout 1 = SWIZZLE_128B_BASE32B (32-bit MN-major
+// operands: 4 k-rows x 128 B atoms, 32-B swizzle granules — TMA's SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t s_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // version = 1 (Blackwell)
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, M=128, N=BN, per-operand major-ness
+__device__ __forceinline__ uint32_t s_idesc(int a_mn_major, int b_mn_major) {
+  uint32_t d = 0;
+  d |= 1u << 4;                    // c_format F32
+  d |= 2u << 7;                    // a_format TF32
+  d |= 2u << 10;                   // b_format TF32
+  d |= (uint32_t)a_mn_major << 15;
+  d |= (uint32_t)b_mn_major << 16;
+  d |= (uint32_t)(S_BN >> 3) << 17;
+  d |= (uint32_t)(S_BM >> 4) << 24;
+  return d;
+}
+
+__global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_constant__ SgemmTask t) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)s_raw + 1023) & ~(uintptr_t)1023);   // SW128 needs 1 KB
+  uint64_t* full = (uint64_t*)(smem + S_STAGES * S_STAGE_BYTES);
+  uint64_t* empty = full + S_STAGES;
+  uint64_t* accum = empty + S_STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (t.h + S_BM - 1) / S_BM;
+  const int m0 = (blockIdx.x % tiles_m) * S_BM, n0 = (blockIdx.x / tiles_m) * S_BN;
+
+  int total = 0;
+  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + S_BK - 1) / S_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S_STAGES; ++s) { s_mbar_init(&full[s], 1); s_mbar_init(&empty[s], 1); }
+    s_mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(tmem_slot)), "n"(S_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  s_fence_before();
+  __syncthreads();
+  s_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int step = 0, k0 = 0;
+      for (int it = 0; it < total; ++it) {
+        const int st = it % S_STAGES;
+        if (it >= S_STAGES) s_mbar_wait(&empty[st], ((it / S_STAGES) - 1) & 1);
+        uint8_t* sa = smem + st * S_STAGE_BYTES;
+        uint8_t* sb = sa + S_A_BYTES;
+        s_mbar_expect_tx(&full[st], S_STAGE_BYTES);
+        const CUtensorMap* ma = &t.steps[step].map_a;
+        const CUtensorMap* mb = &t.steps[step].map_b;
+        if (t.ta) {
+          // A stored K x M (K contiguous): K-major, one box {BK, BM}
+          s_tma_2d(sa, ma, &full[st], k0, m0);
+        } else {
+          // A stored M x K (M contiguous): MN-major, boxes {32 M, BK} stacked every 4 KB
+#pragma unroll
+          for (int i = 0; i < S_BM / 32; ++i) s_tma_2d(sa + i * 4096, ma, &full[st], m0 + 32 * i, k0);
+        }
+        if (!t.tb) {
+          // B stored K x N (K contiguous): K-major, one box {BK, BN}
+          s_tma_2d(sb, mb, &full[st], k0, n0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < S_BN / 32; ++i) s_tma_2d(sb + i * 4096, mb, &full[st], n0 + 32 * i, k0);
+        }
+        k0 += S_BK;
+        if (k0 >= t.steps[step].d) { k0 = 0; ++step; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = s_idesc(!t.ta, t.tb);
+      for (int it = 0; it < total; ++it) {
+        const int st = it % S_STAGES;
+        s_mbar_wait(&full[st], (it / S_STAGES) & 1);
+        s_fence_after();
+        const uint32_t sa = s_u32(smem + st * S_STAGE_BYTES);
+        const uint32_t sb = sa + S_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < S_BK / 8; ++kk) {
+          // K-major: advance 32 B along the swizzled 128-B row; SBO = 8 rows x 128 B.
+          // MN-major: advance 8 k-rows (1 KB); SBO = 4 k-rows (512 B) between k groups,
+          // LBO = 4 KB between the 32-wide MN groups (one TMA box each).
+          const uint64_t da = t.ta ? s_desc(sa + kk * 32, 16, 1024, 2) : s_desc(sa + kk * 1024, t.mn_lbo, t.mn_sbo, 1);
+          const uint64_t db = t.tb ? s_desc(sb + kk * 1024, t.mn_lbo, t.mn_sbo, 1) : s_desc(sb + kk * 32, 16, 1024, 2);
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        // frees the stage once these MMAs have read it
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                     ::"r"(s_u32(&empty[st])) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                   ::"r"(s_u32(accum)) : "memory");
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31  <->  tile rows
+    const int q = warp & 3;
+    const int row = m0 + 32 * q + lane;
+    if (total > 0) {
+      s_mbar_wait(accum, 0);
+      s_fence_after();
+    }
+    for (int c0 = 0; c0 < S_BN; c0 += 16) {
+      uint32_t v[16];
+      if (total > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0u;
+      }
+      if (row < t.h) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = n0 + c0 + i;
+          if (col < t.w) {
+            float* p = t.c + (size_t)col * t.ldc + row;
+            float r = t.alpha * __uint_as_float(v[i]);
+            if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
+            *p = r;
+          }
+        }
+      }
+    }
+  }
+  s_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    s_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(S_TMEM_COLS));
+  }
+}
+
+}  // namespace bx

@@ -256,3 +256,70 @@ if "--launch-overhead" in sys.argv:
         ms = C.c_float()
         lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
         print(f"{label}: host {(t1 - t0) / 50 * 1e6:.1f} us/call, gpu {ms.value / 50 * 1e3:.1f} us/launch")
+
+if "--sgemm" in sys.argv:
+    def put32(arr):
+        arr = np.asfortranarray(arr, dtype=np.float32)
+        h, w = arr.shape
+        ld = (h + 7) // 8 * 8
+        off = _next[0]
+        _next[0] += (ld * w * 4 + 1023) // 1024 * 1024
+        ev = C.c_int(-1)
+        N.check(lib.bx_h2d_tile(0, off, ld, arr.ctypes.data, h, h, w, 4, 0, None, C.byref(ev)), "h2d32")
+        N.check(lib.bx_event_sync(ev.value))
+        return off, ld
+
+    def get32(off, ld, h, w):
+        out = np.empty((h, w), order="F", dtype=np.float32)
+        ev = C.c_int(-1)
+        N.check(lib.bx_d2h_tile(0, off, ld, out.ctypes.data, h, h, w, 4, 0, None, C.byref(ev)), "d2h32")
+        N.check(lib.bx_event_sync(ev.value))
+        return out
+
+    sf = 0
+    for (h, w, d, ns) in [(128, 256, 32, 1), (300, 500, 100, 1), (1024, 1024, 1024, 2), (77, 33, 45, 3)]:
+        for ta in (0, 1):
+            for tb in (0, 1):
+                for beta in (0.0, 0.5):
+                    _next[0] = 0
+                    As = [(rng.random((d, h) if ta else (h, d)) * 2 - 1).astype(np.float32) for _ in range(ns)]
+                    Bs = [(rng.random((w, d) if tb else (d, w)) * 2 - 1).astype(np.float32) for _ in range(ns)]
+                    c = (rng.random((h, w)) * 2 - 1).astype(np.float32)
+                    ref = sum((a.T if ta else a).astype(np.float64) @ (b.T if tb else b).astype(np.float64)
+                              for a, b in zip(As, Bs)) * 1.25 + beta * c.astype(np.float64)
+                    ao, al, bo, bl, dep = [], [], [], [], []
+                    for a, b in zip(As, Bs):
+                        o, l = put32(a); ao.append(o); al.append(l)
+                        o, l = put32(b); bo.append(o); bl.append(l)
+                        dep.append(d)
+                    oc, lc = put32(c)
+                    ev = C.c_int(-1)
+                    N.check(lib.bx_sgemm_task(0, 0, ta, tb, h, w, ns, N.u64_array(ao), N.int_array(al), N.u64_array(bo),
+                                              N.int_array(bl), N.int_array(dep), 1.25, beta, oc, lc, 0, None, C.byref(ev)), "sgemm")
+                    N.check(lib.bx_event_sync(ev.value))
+                    out = get32(oc, lc, h, w).astype(np.float64)
+                    err = np.linalg.norm(out - ref) / np.linalg.norm(ref)
+                    ok = err < 2e-3 and np.isfinite(out).all()
+                    sf += not ok
+                    if not ok:
+                        print("FAIL sgemm", h, w, d, ns, ta, tb, beta, err, np.abs(out - ref).max())
+    print("sgemm fails:", sf)
+    if "--perf" in sys.argv or "--sgemm-perf" in sys.argv:
+        for n in (8192, 16384):
+            ptrs = []
+            for _ in range(3):
+                p = C.c_uint64()
+                N.check(lib.bx_dev_alloc(0, n * n * 4, C.byref(p)))
+                ptrs.append(p.value)
+            for tt in [(0, 0), (0, 1), (1, 0), (1, 1)]:
+                N.check(lib.bx_sgemm_device(0, 0, tt[0], tt[1], n, n, n, 1.0, ptrs[0], n, ptrs[1], n, 0.0, ptrs[2], n))
+                e0, e1 = C.c_int(), C.c_int()
+                lib.bx_event_record(0, 0, 1, C.byref(e0))
+                N.check(lib.bx_sgemm_device(0, 0, tt[0], tt[1], n, n, n, 1.0, ptrs[0], n, ptrs[1], n, 0.0, ptrs[2], n))
+                lib.bx_event_record(0, 0, 1, C.byref(e1))
+                lib.bx_event_sync(e1.value)
+                ms = C.c_float()
+                lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
+                print(f"sgemm_device n={n} trans {tt}: {ms.value:.3f} ms {2*n**3/ms.value/1e9:.1f} TF/s")
+            for p in ptrs:
+                lib.bx_dev_free(0, p)
