@@ -117,7 +117,9 @@ class CudaEngine:
 
     # ---- kernels ------------------------------------------------------------------------
 
-    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=()) -> int:
+    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
+             f32=False) -> int:
+        """One task GEMM launch; ``f32`` selects the tcgen05 TF32 kernel (SGEMM)."""
         n = len(steps)
         a_off = (C.c_uint64 * n)(*[s[0] for s in steps])
         lda = (C.c_int * n)(*[s[1] for s in steps])
@@ -126,6 +128,13 @@ class CudaEngine:
         dep = (C.c_int * n)(*[s[4] for s in steps])
         ev = C.c_int(-1)
         nw, wp = self._waits(waits)
+        if f32:
+            if tri:
+                raise ValueError("the fp32 task GEMM has no triangle mode")
+            N.check(self.lib.bx_sgemm_task(slot, stream, int(ta), int(tb), h, w, n, a_off, lda,
+                                           b_off, ldb, dep, float(alpha), float(beta), c_off, ldc,
+                                           nw, wp, C.byref(ev)), "sgemm task")
+            return ev.value
         N.check(self.lib.bx_gemm_task(slot, stream, int(ta), int(tb), tri, h, w, n, a_off, lda,
                                       b_off, ldb, dep, float(alpha), float(beta), c_off, ldc,
                                       nw, wp, C.byref(ev)), "gemm task")

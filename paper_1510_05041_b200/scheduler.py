@@ -38,7 +38,8 @@ import numpy as np
 from .cache import HOST_FETCH, L1_HIT, L2_HIT, CoherenceDirectory, DeviceTileCache, LruBlock
 from .devices import (DeviceMetrics, Metrics, Topology, TraceEvent, discover_topology,
                       exposed_comm_time)
-from .errors import CapacityDeadlockError, ConfigError, SingularMatrixError
+from .errors import (ArenaOutOfMemoryError, CapacityDeadlockError, ConfigError,
+                     SingularMatrixError)
 from .memory import Arena
 from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
                        TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
@@ -92,12 +93,13 @@ class RunResult:
 
 
 class _SlotEntry:
-    __slots__ = ("task", "release_time", "priority")
+    __slots__ = ("task", "release_time", "priority", "pver")
 
     def __init__(self, task: Task, release_time: float = 0.0):
         self.task = task
         self.release_time = release_time
         self.priority = 0
+        self.pver = -1          # directory version the priority was computed at
 
 
 class ReservationStation:
@@ -243,16 +245,23 @@ class _GpuWorker:
         self._cur: Optional[_Active] = None
         self.plan = runtime.plan
         self.esz = runtime.plan.dtype.itemsize
+        self.f32 = self.esz == 4
         self.tile = runtime.plan.tile_size
         self.trace_on = opts.record_trace
         self.epoch = None
         self._snap_id = runtime.plan.snapshot_alias
         self._permanent = []
         self._retain = opts.retain_outputs and runtime.plan.call.kind == "trsm"
+        self.resident = False   # set by run_plan when the arena holds the whole working set
+        self._sync_epoch = 0
+        self._task_misses = 0
+        self.chunk_steps = opts.chunk_steps
         grp = runtime.topology.peer_group_of(desc)
         self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
                                       if d.device_id != desc.device_id
                                       and runtime.topology.peer_group_of(d) == grp)
+        self._one_group = len(self._group_peers) == len(runtime.topology.devices) - 1
+        self._pending_keys = set()   # resident blocks whose arrival event is not known done
 
     # ---- cache callbacks ------------------------------------------------------------
 
@@ -311,9 +320,10 @@ class _GpuWorker:
         return True
 
     def pressure_sync(self) -> None:
-        """Every cached block is pinned: launch what is pending, drain the GPU, release the
-        pins of all launched work and retire finished tasks, then let the caller retry."""
+        """Every cached block is pinned: drain the GPU, release the pins of all launched work
+        and retire finished tasks, then let the caller retry (cache.py:232-250)."""
         cur = self._cur
+        self._sync_epoch += 1
         self.eng.device_sync(self.slot)
         for act in [a for a in self.active if a is not None] + ([cur] if cur else []):
             for cache, blk in act.launched_pins:
@@ -350,8 +360,17 @@ class _GpuWorker:
         blocks = self.cache._blocks
         holders = self.runtime.directory._holders if self.runtime.options.l2_enabled else None
         group = self._group_peers
+        keys = task_keys(task)
+        if task._bx_single and self._one_group:
+            # every tile referenced once and every GPU in one peer group (NVSwitch):
+            # Eq. 3 = 2 |keys & L1| + |(keys & held anywhere) - L1|, in C-level set ops
+            ks = task._bx_keyset
+            local = ks & blocks.keys()
+            if holders is None:
+                return 2 * len(local)
+            return 2 * len(local) + len((ks & holders.keys()) - local)
         p = 0
-        for key, (_ref, mult) in task_keys(task).items():
+        for key, (_ref, mult) in keys.items():
             if key in blocks:
                 p += 2 * mult
             elif holders is not None:
@@ -362,8 +381,13 @@ class _GpuWorker:
 
     def _next_entry(self):
         self._refill()
+        # Eq. 3 only changes when some cache gains or loses a tile: recompute an entry's
+        # priority only if the directory changed since it was last computed
+        ver = self.runtime.directory.version
         for e in self.rs.entries():
-            e.priority = self._priority(e.task)
+            if e.pver != ver:
+                e.priority = self._priority(e.task)
+                e.pver = ver
         return self.rs.pop_best()
 
     def fill(self) -> bool:
@@ -380,48 +404,147 @@ class _GpuWorker:
 
     # ---- issue ----------------------------------------------------------------------
 
-    def _resolve_task(self, task):
-        """Translate every distinct input tile of a task once (L1 hit / L2 peer copy / host
-        fetch), pin it once for the task, and return key -> (offset, ld, wait).  Hit/miss
-        counters follow the per-reference semantics of the reference translate loop."""
-        act = self._cur
-        out = {}
+    def _resolve_op(self, task, op, res):
+        """Evicting (non-resident) mode: translate and pin only the tiles one launch needs,
+        just before it is enqueued, so a task never needs more than one chunk of inputs in
+        the arena at once (the reference holds one step's tiles, scheduler.py:426-461).
+        If a pressure sync fires meanwhile (pins of launched work released), entries
+        resolved for earlier launches are dropped and re-translated on demand."""
+        keys = task_keys(task)
+        if type(op) is GemmOp:
+            want = [k for ak, bk, _ in op.subs for k in (ak, bk)]
+        else:
+            want = [op.key]
         cache = self.cache
-        blocks = cache._blocks
-        for key, (ref, mult) in task_keys(task).items():
-            with cache.lock:
-                blk = blocks.get(key)
-                if blk is not None:
-                    blocks.move_to_end(key)
-                    blk.reader += 1
-            if blk is not None:
-                self.l1_hits += mult
-            else:
+        for _attempt in range(4):
+            epoch = self._sync_epoch
+            pinned_now = set()
+            restart = False
+            for key in want:
+                if key in res or key[0] == "#scratch":
+                    continue
+                ref = keys[key][0]
                 h, w, ld, nbytes = self._tile_geom(ref)
                 blk, outcome = cache.translate(ref, self, nbytes=nbytes, ld=ld)
-                if outcome == L1_HIT:
-                    self.l1_hits += mult
-                else:
-                    if outcome == L2_HIT:
-                        self.l2_hits += 1
-                    else:
-                        self.host_fetches += 1
-                    self.l1_hits += mult - 1
+                if outcome == L2_HIT:
+                    self.l2_hits += 1
+                    self._task_misses += 1
+                elif outcome == HOST_FETCH:
+                    self.host_fetches += 1
+                    self._task_misses += 1
                 cache.pin(blk)
-                if key[0] == self._snap_id:
-                    # aliased TRMM snapshot tile: keep it resident for the whole call so
-                    # nobody re-fetches it from host after its owner wrote it back
-                    cache.pin(blk)
-                    self._permanent.append(blk)
-            act.pins.append((cache, blk))
+                self._cur.pins.append((cache, blk))
+                pinned_now.add(key)
+                wait = None
+                if blk.ready_ev is not None and not blk.ready_done:
+                    if self.eng.done(blk.ready_ev):
+                        blk.ready_done = True
+                    else:
+                        wait = blk.ready_ev
+                res[key] = (blk.offset, blk.ld, wait)
+                if self._sync_epoch != epoch:
+                    restart = True
+                    break
+            if not restart:
+                return res
+            # launched pins were released by the drain: keep only what is pinned now
+            for k in list(res):
+                if k not in pinned_now and k[0] != "#scratch":
+                    del res[k]
+        raise CapacityDeadlockError(
+            f"device {self.device_id}: one launch's tiles cannot all fit in the arena at once; "
+            f"enlarge the arena or shrink the tiles")
+
+    def _resolve_resident(self, task):
+        """Resident mode: the arena was sized to hold every input tile of the call, so the
+        ALRU can never evict.  Each block is pinned once, permanently, when it arrives, and
+        a task's translation reduces to lookups (no per-task pins / recency updates)."""
+        cache = self.cache
+        blocks = cache._blocks
+        keys = task_keys(task)
+        ks = task._bx_keyset
+        pend = self._pending_keys
+        if pend and not pend.isdisjoint(ks):
+            # drop keys whose copies have landed
+            eng = self.eng
+            for k in list(pend & ks):
+                b = blocks.get(k)
+                if b is None or b.ready_done or eng.done(b.ready_ev):
+                    if b is not None:
+                        b.ready_done = True
+                    pend.discard(k)
+        if ks <= blocks.keys() and pend.isdisjoint(ks):
+            # steady state: every tile resident and landed
+            self.l1_hits += task._bx_refs
+            return {k: (b.offset, b.ld, None) for k in ks for b in (blocks[k],)}
+        out = {}
+        eng = self.eng
+        hits = 0
+        for key, (ref, mult) in keys.items():
+            blk = blocks.get(key)
+            if blk is None:
+                blk = self._fetch_resident(key, ref)
+                hits += mult - 1
+            else:
+                hits += mult
             wait = None
-            if blk.ready_ev is not None and not blk.ready_done:
-                if self.eng.done(blk.ready_ev):
+            ev = blk.ready_ev
+            if ev is not None and not blk.ready_done:
+                if eng.done(ev):
                     blk.ready_done = True
                 else:
-                    wait = blk.ready_ev
+                    wait = ev
+                    pend.add(key)
             out[key] = (blk.offset, blk.ld, wait)
+        self.l1_hits += hits
         return out
+
+    def _fetch_resident(self, key, ref):
+        """Miss path of resident mode: allocate (never evicts), copy from the lowest-id peer
+        holding the tile (L2 over NVLink) or from pinned host memory, register the block
+        in the directory and pin it for the call."""
+        h, w = ref.phys_height, ref.phys_width
+        ld = device_ld(h)
+        nbytes = ld * w * self.esz
+        try:
+            off = self.arena.alloc(nbytes)
+        except ArenaOutOfMemoryError:
+            raise CapacityDeadlockError(
+                f"device {self.device_id}: resident arena exhausted (working-set estimate "
+                f"too small); set DeviceDesc.arena_capacity to use the evicting cache") from None
+        blk = LruBlock(key, off, nbytes, ld, self.device_id)
+        blk.reader = 1
+        payload = h * w * self.esz
+        directory = self.runtime.directory
+        src_id = directory.peer_source(key, self.device_id) if self.runtime.options.l2_enabled else None
+        src_blk = None
+        if src_id is not None:
+            src_blk = directory.cache_of(src_id)._blocks.get(key)
+        if src_blk is not None:
+            waits = ()
+            if src_blk.ready_ev is not None and not src_blk.ready_done:
+                if self.eng.done(src_blk.ready_ev):
+                    src_blk.ready_done = True
+                else:
+                    waits = (src_blk.ready_ev,)
+            src_slot = self.eng.slot(src_id)
+            blk.ready_ev = self._timed(LANE_P2P, lambda wt: self.eng.p2p(
+                self.slot, off, src_slot, src_blk.offset, nbytes, wt), waits, "D2D", payload)
+            self.dm.d2d_in_bytes += payload
+            self.runtime.add_d2d_out(src_id, payload)
+            self.l2_hits += 1
+        else:
+            desc, r0, c0 = self._host_of(ref)
+            blk.ready_ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(
+                self.slot, off, ld, desc, r0, c0, h, w, wt), (), "H2D", payload)
+            self.dm.h2d_bytes += payload
+            self.host_fetches += 1
+        self._pending_keys.add(key)
+        with self.cache.lock:
+            self.cache._blocks[key] = blk
+        directory.add_holder(key, self.device_id)
+        self._permanent.append(blk)
+        return blk
 
     def _resolve_uncached(self, task):
         """l1_enabled=False (scheduler.py:463-485): every step reference is a fresh host
@@ -477,33 +600,33 @@ class _GpuWorker:
                 act.events.append(ev)
                 act.pending_waits.append(ev)
                 self.dm.h2d_bytes += h * w * self.esz
-            prog = compile_task(task, call, opts.chunk_steps, opts.first_chunk_steps)
-            if opts.l1_enabled:
-                res = self._resolve_task(task)
-            else:
+            prog = compile_task(task, call, self.chunk_steps, opts.first_chunk_steps)
+            lazy = opts.l1_enabled and not self.resident
+            self._task_misses = 0
+            if not opts.l1_enabled:
                 res = self._resolve_uncached(task)
+            elif self.resident:
+                res = self._resolve_resident(task)
+            else:
+                res = {}
             for i, n in enumerate(prog.scratch_n):
                 ld = device_ld(n)
                 off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
                 act.scratch.append(off)
                 res[scratch_key(i)] = (off, ld, None)
             for op in prog.ops:
+                if lazy:
+                    res = self._resolve_op(task, op, res)
                 if type(op) is GemmOp:
-                    steps = []
-                    waits = []
-                    for ak, bk, d in op.subs:
-                        ao, al, aw = res[ak]
-                        bo, bl, bw = res[bk]
-                        steps.append((ao, al, bo, bl, d))
-                        if aw is not None and aw not in waits:
-                            waits.append(aw)
-                        if bw is not None and bw not in waits:
-                            waits.append(bw)
+                    ops_ = [(res[ak], res[bk], d) for ak, bk, d in op.subs]
+                    steps = [(a[0], a[1], b[0], b[1], d) for a, b, d in ops_]
+                    waits = list(dict.fromkeys(
+                        w_ for a, b, _ in ops_ for w_ in (a[2], b[2]) if w_ is not None))
                     waits += act.pending_waits
                     act.pending_waits = []
                     ev = self._timed(stream, lambda wt, op=op, steps=steps: eng.gemm(
                         slot, stream, op.ta, op.tb, op.tri, h, w, steps, op.alpha, op.beta,
-                        act.c_off, act.c_ld, wt), waits, "KERNEL", op.flops, op.k)
+                        act.c_off, act.c_ld, wt, f32=self.f32), waits, "KERNEL", op.flops, op.k)
                     self._launched(act, ev)
                 elif type(op) is MatOp:
                     ao, al, aw = res[op.key]
@@ -531,6 +654,8 @@ class _GpuWorker:
             self.dm.d2h_bytes += h * w * self.esz
             act.events.append(act.done_ev)
             act.flops = task.flops
+            if lazy:
+                self.l1_hits += task._bx_refs - self._task_misses
         finally:
             self._cur = None
         self.active[slot_index] = act
@@ -560,6 +685,9 @@ class _GpuWorker:
                            self.device_id)
             blk.ready_done = True
             self.cache.insert_front(blk)
+            if self.resident:
+                self.cache.pin(blk)
+                self._permanent.append(blk)
         else:
             self.arena.free(act.c_off)
         if self.plan.call.kind == "trsm" and self.eng.singular(self.slot, reset=True):
@@ -595,7 +723,8 @@ class _GpuWorker:
 
 def task_keys(task: Task) -> dict:
     """Distinct input tiles of a task: key -> (ref, number of step references).  Cached on
-    the (immutable) task."""
+    the (immutable) task together with its key set, total reference count and whether
+    every tile is referenced once (the set-arithmetic priority fast path)."""
     keys = getattr(task, "_bx_keys", None)
     if keys is None:
         keys = {}
@@ -605,6 +734,9 @@ def task_keys(task: Task) -> dict:
                 hit = keys.get(k)
                 keys[k] = (ref if hit is None else hit[0], 1 if hit is None else hit[1] + 1)
         task._bx_keys = keys
+        task._bx_keyset = frozenset(keys)
+        task._bx_refs = sum(m for _, m in keys.values())
+        task._bx_single = task._bx_refs == len(keys)
     return keys
 
 
@@ -651,14 +783,17 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     esz = plan.dtype.itemsize
     per_tile = device_ld(plan.tile_size) * plan.tile_size * esz
     caps = {}
+    resident = {}
     for d in devs:
         slot = engine.slot(d.device_id)
         want = d.arena_capacity or options.arena_bytes
+        resident[slot] = not want
         if not want:
-            want = _auto_arena_bytes(plan, options, None)
+            full = want = _auto_arena_bytes(plan, options, None)
             if want > engine.arena_capacity(slot):     # only then ask the driver (slow query)
                 want = _auto_arena_bytes(plan, options, engine.free_bytes(slot)
                                          + engine.arena_capacity(slot))
+            resident[slot] = want >= full              # out-of-core calls keep the full ALRU
         if want <= WORKING_SET_TILES * per_tile:
             raise ConfigError(
                 f"device {d.device_id}: arena of {want} bytes cannot hold the "
@@ -686,6 +821,12 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     rt = _Runtime(plan, topology, options, engine)
     workers = [_GpuWorker(d, rt) for d in devs]
     for w in workers:
+        w.resident = resident[w.slot] and options.l1_enabled
+        if not w.resident:
+            # an evicting arena must hold every in-flight task's C and one launch's inputs
+            tiles = caps[w.slot] // per_tile
+            inflight = options.n_streams * options.tasks_per_stream
+            w.chunk_steps = max(1, min(options.chunk_steps, (tiles - 2 * inflight) // 4))
         # an explicit capacity smaller than the reservation bounds the arena (eviction tests)
         if caps[w.slot] < w.arena.capacity:
             w.arena = Arena(caps[w.slot])

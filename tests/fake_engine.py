@@ -62,7 +62,7 @@ class FakeEngine:
         return dict(name="fake", sms=148, total_bytes=1 << 34, free_bytes=self.default_arena)
 
     def free_bytes(self, slot):
-        return self.default_arena
+        return self.default_arena + (2 << 30)
 
     def ensure_arenas(self, caps):
         for slot, c in caps.items():
@@ -122,15 +122,25 @@ class FakeEngine:
         assert base + ld * w <= a.size, "access outside arena"
         return a[base:base + ld * w].reshape(w, ld).T[:h, :]
 
+    def _view32(self, slot, off, ld, h, w):
+        a = self.arenas[slot].view(np.float32)
+        assert off % 4 == 0
+        base = off // 4
+        assert base + ld * w <= a.size, "access outside arena"
+        return a[base:base + ld * w].reshape(w, ld).T[:h, :]
+
+    def _viewT(self, slot, off, ld, h, w, esz):
+        return self._view32(slot, off, ld, h, w) if esz == 4 else self._view(slot, off, ld, h, w)
+
     # ---- transfers ----
     def h2d(self, slot, dst_off, dst_ld, desc, r0, c0, h, w, waits=()):
         def fn():
-            self._view(slot, dst_off, dst_ld, h, w)[:, :] = desc.as_2d()[r0:r0 + h, c0:c0 + w]
+            self._viewT(slot, dst_off, dst_ld, h, w, desc.itemsize)[:, :] = desc.as_2d()[r0:r0 + h, c0:c0 + w]
         return self._enqueue(slot, -1, fn, waits)
 
     def d2h(self, slot, src_off, src_ld, desc, r0, c0, h, w, waits=()):
         def fn():
-            desc.as_2d()[r0:r0 + h, c0:c0 + w] = self._view(slot, src_off, src_ld, h, w)
+            desc.as_2d()[r0:r0 + h, c0:c0 + w] = self._viewT(slot, src_off, src_ld, h, w, desc.itemsize)
         return self._enqueue(slot, -2, fn, waits)
 
     def p2p(self, dst_slot, dst_off, src_slot, src_off, nbytes, waits=()):
@@ -140,15 +150,17 @@ class FakeEngine:
         return self._enqueue(dst_slot, -3, fn, waits)
 
     # ---- kernels ----
-    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=()):
+    def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
+             f32=False):
         self.n_launches += 1
+        view = self._view32 if f32 else self._view
 
         def fn():
-            c = self._view(slot, c_off, ldc, h, w)
+            c = view(slot, c_off, ldc, h, w)
             acc = np.zeros((h, w))
             for (ao, lda, bo, ldb, d) in steps:
-                a = self._view(slot, ao, lda, d if ta else h, h if ta else d)
-                b = self._view(slot, bo, ldb, w if tb else d, d if tb else w)
+                a = view(slot, ao, lda, d if ta else h, h if ta else d)
+                b = view(slot, bo, ldb, w if tb else d, d if tb else w)
                 acc += (a.T if ta else a) @ (b.T if tb else b)
             new = alpha * acc if beta == 0.0 else alpha * acc + beta * c
             if tri:

@@ -205,3 +205,34 @@ def test_concurrent_mode_and_trace():
     assert any(e.event == "KERNEL" for e in res.trace)
     ks = [e for e in res.trace if e.event == "KERNEL"]
     assert all(e.time_end >= e.time_start for e in ks)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_sgemm_tcgen05_against_fp64_oracle(ta, tb):
+    """SGEMM has no reference path (tiling.py:57-60 is float64 only): compare with the
+    float64 tiled oracle on the same float32-representable inputs, eps = 2^-23."""
+    call = build_call("gemm", m=1500, n=1300, k=1100, tile_size=512, seed=11, alpha=1.0, beta=0.5,
+                      trans_a=ta, trans_b=tb, dtype=np.float32)
+    a = call.a.matrix.as_2d().astype(np.float64)
+    b = call.b.matrix.as_2d().astype(np.float64)
+    c0 = call.c.matrix.as_2d().astype(np.float64)
+    run_call(call)
+    out = call.c.matrix.as_2d().astype(np.float64)
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=512, alpha=1.0, beta=0.5, trans_a=ta, trans_b=tb)
+    r = tolerance.gemm_ratio(out, ref, a_norm=np.linalg.norm(a), b_norm=np.linalg.norm(b), k=1100,
+                             alpha=1.0, beta=0.5, c0_norm=np.linalg.norm(c0),
+                             eps=float(np.finfo(np.float32).eps))
+    assert r <= tolerance.BOUND, r
+
+
+def test_cblas_sgemm():
+    from paper_1510_05041_b200 import sgemm
+    rng = np.random.default_rng(4)
+    m, n, k = 700, 600, 500
+    a = np.asfortranarray(rng.random((m, k), dtype=np.float32))
+    b = np.asfortranarray(rng.random((k, n), dtype=np.float32))
+    c = np.asfortranarray(np.zeros((m, n), dtype=np.float32))
+    sgemm("N", "N", m, n, k, 1.0, a, m, b, k, 0.0, c, m, tile_size=256)
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    assert np.linalg.norm(c - ref) / np.linalg.norm(ref) < 1e-3

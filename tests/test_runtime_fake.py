@@ -158,3 +158,35 @@ def test_stealing_feeds_idle_device():
     assert S.steal_for(w1) is None                # queue not empty -> no theft
     rt.queue.get()
     assert S.steal_for(w1) is not None and S.steal_for(w1) is None   # victim keeps its last
+
+
+def test_sgemm_plan_runs_in_fp32():
+    call = build_call("gemm", m=40, n=24, k=36, tile_size=16, seed=6, beta=0.5,
+                      dtype=np.float32, trans_b=True)
+    a = call.a.matrix.as_2d().astype(np.float64)
+    b = call.b.matrix.as_2d().astype(np.float64)
+    c0 = call.c.matrix.as_2d().astype(np.float64)
+    run_call(call, topo(2), RunOptions(), engine=FakeEngine(2))
+    np.testing.assert_allclose(call.c.matrix.as_2d(), a @ b.T + 0.5 * c0, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("kind", ["gemm", "trsm", "trmm", "syr2k"])
+def test_resident_mode_multi_device(kind):
+    """arena_capacity=0 lets the runtime size the arena for the whole working set
+    (resident mode: permanent pins, no per-task ALRU bookkeeping)."""
+    call = build_call(kind, m=48, n=40, k=32, tile_size=8, seed=12, beta=0.5, uplo="lower",
+                      trsm_scaled=True)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    topo = Topology([DeviceDesc(i, arena_capacity=0, peer_group="g") for i in range(3)])
+    res = run_call(call, topo, RunOptions(), engine=FakeEngine(3, seed=5, arena_bytes=1 << 26))
+    from oracle import tiled
+    ref = c0.copy()
+    tiled.run_tiled(kind, a, ref, b, tile_size=8, alpha=1.0, beta=0.0 if kind in ("trsm", "trmm") else 0.5,
+                    uplo="lower")
+    np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-11, atol=1e-11)
+    m = res.metrics
+    assert m.total_d2d_bytes() == sum(d.d2d_out_bytes for d in m.devices.values())
+    if kind == "gemm":
+        assert m.l2_hits > 0

@@ -65,11 +65,17 @@ call = RoutineCall("gemm", a=tm("A"), b=tm("B"), c=tm("C"), beta=1.0)
 topo = Topology([DeviceDesc(d, peer_group="g") for d in range(ndev)])
 eng = NullEngine(ndev)
 opts = RunOptions(chunk_steps=chunk)
-t0 = time.perf_counter()
-res = run_call(call, topo, opts, engine=eng)
-dt = time.perf_counter() - t0
+best = None
+for _ in range(5):
+    t0 = time.perf_counter()
+    r = run_call(call, topo, opts, engine=NullEngine(ndev))
+    d = time.perf_counter() - t0
+    if best is None or d < best[0]:
+        best = (d, r)
+dt, res = best
 print(f"n={n} T={t} ndev={ndev}: {len(res.plan.tasks)} tasks, host time {dt*1e3:.1f} ms "
-      f"= {dt/len(res.plan.tasks)*1e6:.0f} us/task; l2 hits {res.metrics.l2_hits}")
+      f"= {dt/len(res.plan.tasks)*1e6:.0f} us/task; l2 hits {res.metrics.l2_hits}; phases "
+      f"{ {k: round(v * 1e3, 1) for k, v in res.metrics.phases.items()} }")
 if "--prof" in sys.argv:
     cProfile.run("run_call(call, topo, opts, engine=NullEngine(ndev))", "/tmp/hostprof")
     pstats.Stats("/tmp/hostprof").sort_stats("tottime").print_stats(18)
