@@ -54,7 +54,7 @@ struct Device {
   std::vector<cudaEvent_t> events;  // id -> event
   std::vector<int> timing;          // whether created with timing
   std::vector<int> free_sync, free_timing;
-  unsigned attr_set = 0;  // cudaFuncSetAttribute done on this device (bit per kernel)
+  std::vector<const void*> attr_set;  // kernels whose smem attribute is set on this device
   bool ready = false;
 };
 
@@ -140,11 +140,13 @@ int current_dev_slot() {
 }
 
 // cudaFuncSetAttribute is per device: remember which kernels were configured where.
-bool need_attr(unsigned bit) {
+bool need_attr(const void* kernel) {
   int d = current_dev_slot();
   if (d < 0) return true;
-  if (g_devs[d].attr_set & bit) return false;
-  g_devs[d].attr_set |= bit;
+  auto& v = g_devs[d].attr_set;
+  for (const void* k : v)
+    if (k == kernel) return false;
+  v.push_back(kernel);
   return true;
 }
 
@@ -152,8 +154,8 @@ int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
 int g_trsm_leaf = 128;   // triangle order solved by a leaf kernel; larger ones recurse
 
 template <class Cfg, bool TA, bool TB>
-int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
-  if (need_attr(bit)) {
+int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s) {
+  if (need_attr((const void*)bx::gemm_task_kernel<Cfg, TA, TB>)) {
     CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Cfg::SMEM_BYTES));
   }
@@ -165,8 +167,8 @@ int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
 }
 
 template <class Cfg, bool TA, bool TB>
-int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
-  if (need_attr(bit)) {
+int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s) {
+  if (need_attr((const void*)bx::gemm_task_mb_kernel<Cfg, TA, TB>)) {
     CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_mb_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Cfg::SMEM_BYTES));
   }
@@ -179,15 +181,16 @@ int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s, unsigned bit) {
 
 template <bool TA, bool TB>
 int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
-  unsigned tb = (TA ? 2u : 0u) + (TB ? 1u : 0u);
   switch (g_gemm_variant) {
-    case 1: return launch_gemm_cfg<bx::CfgWide, TA, TB>(t, s, 1u << (16 + tb));
-    case 2: return launch_gemm_cfg<bx::CfgDeep, TA, TB>(t, s, 1u << (24 + tb));
-    case 3: return launch_gemm_ws<bx::CfgMb2, TA, TB>(t, s, 1u << (20 + tb));
-    case 4: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s, 1u << (28 + tb));
-    case 5: return launch_gemm_ws<bx::CfgMbPair, TA, TB>(t, s, 1u << (4 + tb));
-    case 6: return launch_gemm_ws<bx::CfgMbPairS, TA, TB>(t, s, 1u << (0 + tb));
-    default: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s, 1u << (12 + tb));
+    case 1: return launch_gemm_cfg<bx::CfgWide, TA, TB>(t, s);
+    case 2: return launch_gemm_cfg<bx::CfgDeep, TA, TB>(t, s);
+    case 3: return launch_gemm_ws<bx::CfgMb2, TA, TB>(t, s);
+    case 4: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s);
+    case 5: return launch_gemm_ws<bx::CfgMbPair, TA, TB>(t, s);
+    case 6: return launch_gemm_ws<bx::CfgMbK32, TA, TB>(t, s);
+    case 7: return launch_gemm_ws<bx::CfgMbS0, TA, TB>(t, s);
+    case 99: return launch_gemm_ws<bx::CfgMbNoLoad, TA, TB>(t, s);
+    default: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s);
   }
 }
 
@@ -286,7 +289,7 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
       else rc = tensor_map_f32(b[j], w, d, ldb[j], 32, 32, MN, &t.steps[i].map_b);
       if (rc) return rc;
     }
-    if (need_attr(1u << 9)) {
+    if (need_attr((const void*)bx::sgemm_tc_kernel)) {
       CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::S_SMEM_BYTES));
     }
     int tiles = ((h + bx::S_BM - 1) / bx::S_BM) * ((w + bx::S_BN - 1) / bx::S_BN);
@@ -363,7 +366,7 @@ int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int
     return BX_OK;
   }
   size_t smem = (size_t)t.n * bx::T_YP * sizeof(double);
-  if (need_attr(1u << 8)) {
+  if (need_attr((const void*)bx::trsm_panel_kernel)) {
     CUDA_TRY(cudaFuncSetAttribute(bx::trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   bx::T_NMAX * bx::T_YP * (int)sizeof(double)));
   }

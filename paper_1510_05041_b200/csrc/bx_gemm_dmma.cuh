@@ -223,9 +223,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_kernel(const __grid
 // ---------------------------------------------------------------------------------------
 namespace bx {
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int SLACK_, int MINB_ = 1>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int SLACK_, int MINB_ = 1, bool NOLOAD_ = false>
 struct MbCfg : GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_> {
   using Base = GemmCfg<BM_, BN_, BK_, WM_, WN_, STAGES_>;
+  static constexpr bool NOLOAD = NOLOAD_;   // experiment: skip global loads after the first ring
   static constexpr int SLACK = SLACK_;
   static constexpr int MIN_BLOCKS = MINB_;   // CTAs per SM the register budget targets
   static constexpr int DIST = STAGES_ - 1 - SLACK_;   // prefetch distance in slabs
@@ -239,6 +240,9 @@ using CfgMb2 = MbCfg<128, 128, 16, 64, 32, 5, 2>;   // more slack, shorter prefe
 using CfgMb16 = MbCfg<128, 128, 16, 32, 32, 5, 1>;  // 16 warps (4 per SMSP)
 // two CTAs per SM (4 warps each): one CTA's stage hand-offs hide behind the other's DMMAs
 using CfgMbPair = MbCfg<64, 128, 16, 32, 64, 3, 0, 2>;
+using CfgMbK32 = MbCfg<128, 128, 32, 64, 32, 3, 0>;    // BK 32, 3 stages (221 KB)
+using CfgMbS0 = MbCfg<128, 128, 16, 64, 32, 5, 0>;     // no slack, prefetch distance 4
+using CfgMbNoLoad = MbCfg<128, 128, 16, 64, 32, 5, 1, 1, true>;   // experiment only
 using CfgMbPairS = MbCfg<64, 128, 16, 32, 64, 3, 1, 2>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -254,8 +258,46 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// one contiguous global -> shared bulk copy whose bytes complete_tx on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_full(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+template <class Cfg, int EXT, bool KCONTIG>
+__device__ __forceinline__ void fast_slab(double* s, const double* g, int ld, int mn0, int k0, int tid) {
+  constexpr int BK = Cfg::BK;
+  constexpr int PER = (EXT * BK / 2) / Cfg::THREADS;
+  if (KCONTIG) {
+    constexpr int KCH = BK / 2;
+    constexpr int ROWS = Cfg::THREADS / KCH;       // mn rows covered per pass
+    const int mn = tid / KCH, k = (tid % KCH) * 2;
+    const double* src = g + (size_t)(mn0 + mn) * ld + k0 + k;
+    double* dst = s + mn * Cfg::LD_K + k;
+#pragma unroll
+    for (int c = 0; c < PER; ++c)
+      cp_async16_full(dst + c * ROWS * Cfg::LD_K, src + (size_t)c * ROWS * ld);
+  } else {
+    constexpr int MCH = EXT / 2;
+    constexpr int KR = Cfg::THREADS / MCH;         // k rows covered per pass
+    const int k = tid / MCH, mn = (tid % MCH) * 2;
+    const double* src = g + (size_t)(k0 + k) * ld + mn0 + mn;
+    double* dst = s + k * (EXT + 4) + mn;
+#pragma unroll
+    for (int c = 0; c < PER; ++c)
+      cp_async16_full(dst + c * KR * (EXT + 4), src + (size_t)c * KR * ld);
+  }
 }
 
 template <class Cfg, bool TA, bool TB>
@@ -284,6 +326,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  int total = 0;
+  bool kfull = true;
+  for (int s = 0; s < t.nsteps; ++s) {
+    total += (t.steps[s].d + BK - 1) / BK;
+    kfull = kfull && (t.steps[s].d % BK == 0);
+  }
+  // Interior CTAs (no tile edge in m, n or any step's k) take an unpredicated cp.async
+  // path with no bounds arithmetic; edge CTAs keep the zero-filling path.
+  const bool bulk = kfull && m0 + BM <= t.h && n0 + BN <= t.w && !Cfg::NOLOAD;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], Cfg::THREADS);
@@ -292,17 +344,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   }
   __syncthreads();
 
-  int total = 0;
-  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + BK - 1) / BK;
-
   int ld_step = 0, ld_k = 0;
   auto produce = [&](int slab) {
     const int stage = slab % STAGES;
     if (slab >= STAGES) mbar_wait(&empty[stage], ((slab / STAGES) - 1) & 1);
     const GemmStep& st = t.steps[ld_step];
-    load_slab<Cfg, BM, A_KMAJ>(sA + stage * Cfg::A_ELEMS, st.a, st.lda, m0, t.h, ld_k, st.d, tid);
-    load_slab<Cfg, BN, B_KMAJ>(sB + stage * Cfg::B_ELEMS, st.b, st.ldb, n0, t.w, ld_k, st.d, tid);
-    cp_async_arrive_noinc(&full[stage]);
+    if (bulk) {
+      fast_slab<Cfg, BM, A_KMAJ>(sA + stage * Cfg::A_ELEMS, st.a, st.lda, m0, ld_k, tid);
+      fast_slab<Cfg, BN, B_KMAJ>(sB + stage * Cfg::B_ELEMS, st.b, st.ldb, n0, ld_k, tid);
+      cp_async_arrive_noinc(&full[stage]);
+    } else {
+      if (!Cfg::NOLOAD || slab < STAGES) {
+        load_slab<Cfg, BM, A_KMAJ>(sA + stage * Cfg::A_ELEMS, st.a, st.lda, m0, t.h, ld_k, st.d, tid);
+        load_slab<Cfg, BN, B_KMAJ>(sB + stage * Cfg::B_ELEMS, st.b, st.ldb, n0, t.w, ld_k, st.d, tid);
+      }
+      cp_async_arrive_noinc(&full[stage]);
+    }
     ld_k += BK;
     if (ld_k >= st.d) { ld_k = 0; ++ld_step; }
   };
@@ -351,10 +408,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
           for (int j = 0; j < NF; ++j) fb[nx][j] = frag<Cfg, BN, B_KMAJ>(b2, wn + j * 8 + g, q);
         }
       }
+      // serpentine order: consecutive DMMAs share an operand register (operand reuse)
 #pragma unroll
       for (int i = 0; i < MF; ++i)
 #pragma unroll
-        for (int j = 0; j < NF; ++j) dmma(acc[i][j], fa[cur][i], fb[cur][j]);
+        for (int jj = 0; jj < NF; ++jj) {
+          const int j = (i & 1) ? NF - 1 - jj : jj;
+          dmma(acc[i][j], fa[cur][i], fb[cur][j]);
+        }
     }
   }
   cp_async_wait<0>();
