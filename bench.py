@@ -50,6 +50,10 @@ CONFIGS = {
                       uplo="lower", desc="DTRSM left/lower/notrans 16384, tile 1024 (configs[3])"),
     "cfg4_trmm": dict(kind="trmm", m=16384, n=16384, k=16384, tile=1024, alpha=1.0, beta=0.0,
                       uplo="lower", desc="DTRMM left/lower/notrans 16384, tile 1024 (configs[3])"),
+    "cfg5_sgemm": dict(kind="gemm", m=32768, n=32768, k=32768, tile=2048, alpha=1.0, beta=1.0,
+                       dtype="f32", sweep=(512, 1024, 2048, 4096),
+                       desc="SGEMM 32768^3 NN host-resident on tcgen05 (TF32), tile 2048 + tile sweep "
+                            "512-4096 (BASELINE configs[4])"),
 }
 METRIC = "DGEMM TFLOP/s at 1/2/4/8 B200 (host-resident operands), % of FP64 peak"
 
@@ -119,14 +123,37 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- helpers
 
-def make_operands(cfg, seed=0):
+def make_operands(cfg, seed=0, tile=None):
     from paper_1510_05041_b200.operands import build_call
     kw = {}
     if "uplo" in cfg:
         kw["uplo"] = cfg["uplo"]
-    return build_call(cfg["kind"], m=cfg["m"], n=cfg["n"], k=cfg["k"], tile_size=cfg["tile"],
+    if cfg.get("dtype") == "f32":
+        kw["dtype"] = np.float32
+    return build_call(cfg["kind"], m=cfg["m"], n=cfg["n"], k=cfg["k"], tile_size=tile or cfg["tile"],
                       seed=seed, alpha=cfg["alpha"], beta=cfg["beta"],
                       trsm_scaled=cfg["kind"] in ("trsm", "trmm"), **kw)
+
+
+def retile(call, tile):
+    """Same operands, another tile size."""
+    from paper_1510_05041_b200 import RoutineCall
+    from paper_1510_05041_b200.tiling import make_tiled
+    return RoutineCall(call.kind, a=make_tiled(call.a.matrix, tile),
+                       b=None if call.b is None else make_tiled(call.b.matrix, tile),
+                       c=make_tiled(call.c.matrix, tile), alpha=call.alpha, beta=call.beta,
+                       trans_a=call.trans_a, trans_b=call.trans_b, uplo=call.uplo, side=call.side,
+                       diag=call.diag)
+
+
+def tf32_peak_tflops():
+    """tcgen05 kind::tf32 issues at half the kind::f16 rate: use half of the driver-measured
+    dense bf16 peak (MEASURED_PEAKS.json), else half of the profiling guide's fallback."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return mp["bf16_tflops"] / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2 (kind::tf32 = half the f16 rate)"
+    except (OSError, ValueError, KeyError):
+        return 1590.0 / 2.0, "fallback 1.59 PF bf16 / 2 (B200_PROFILING.md)"
 
 
 def cpu_sample(cfg, call, target_s=12.0):
@@ -199,6 +226,8 @@ def device_value_leg(args, cfg, eng, lib, N):
     """Device-resident DGEMM of the same shape, sharded by column panels over the GPUs."""
     from paper_1510_05041_b200 import _native as NN
     m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    f32 = cfg.get("dtype") == "f32"
+    esz = 4 if f32 else 8
     ngpu = args.gpus
     cols = [n // ngpu + (1 if g < n % ngpu else 0) for g in range(ngpu)]
     bufs = []
@@ -207,8 +236,11 @@ def device_value_leg(args, cfg, eng, lib, N):
         ptrs = []
         for nelem in (m * k, k * cols[g], m * cols[g]):
             p = C.c_uint64()
-            NN.check(lib.bx_dev_alloc(slot, nelem * 8, C.byref(p)), "alloc")
-            NN.check(lib.bx_dev_fill_uniform(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
+            NN.check(lib.bx_dev_alloc(slot, nelem * esz, C.byref(p)), "alloc")
+            if f32:
+                NN.check(lib.bx_dev_fill_uniform_f32(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
+            else:
+                NN.check(lib.bx_dev_fill_uniform(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
             ptrs.append(p.value)
         bufs.append(ptrs)
     for g in range(ngpu):
@@ -217,7 +249,10 @@ def device_value_leg(args, cfg, eng, lib, N):
     def launch(g):
         s = eng.slot(g)
         a, b, c = bufs[g]
-        NN.check(lib.bx_dgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
+        if f32:
+            NN.check(lib.bx_sgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 0.0, c, m), "sgemm")
+        else:
+            NN.check(lib.bx_dgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
 
     for _ in range(args.warmup):
         for g in range(ngpu):
@@ -286,7 +321,23 @@ def e2e_leg(args, cfg, eng):
     ms = statistics.mean(times)
     flops = res.plan.total_flops
     mt = metrics[-1]
-    return dict(value=flops / (ms / 1e3) / 1e12, ms=ms, flops=flops, launches=launches,
+    sweep = []
+    for t in cfg.get("sweep", ()):
+        c2 = retile(call, t)
+        run_call(c2, topo, opts)
+        e0 = eng.record(0, 0, timing=True)
+        r2 = run_call(c2, topo, opts)
+        e1 = eng.record(0, 0, timing=True)
+        eng.sync(e1)
+        tms = eng.elapsed_ms(e0, e1)
+        eng.release(e0)
+        eng.release(e1)
+        m2 = r2.metrics
+        sweep.append(dict(tile=t, ms=tms, tflops=flops / (tms / 1e3) / 1e12,
+                          h2d_bytes=m2.total_h2d_bytes(), p2p_bytes=m2.total_d2d_bytes(),
+                          d2h_bytes=m2.total_d2h_bytes(), tasks=len(r2.plan.tasks),
+                          l1_hits=m2.l1_hits, l2_hits=m2.l2_hits, host_fetches=m2.host_fetches))
+    return dict(value=flops / (ms / 1e3) / 1e12, ms=ms, flops=flops, launches=launches, sweep=sweep,
                 h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(), p2p=mt.total_d2d_bytes(),
                 l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
                 per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
@@ -324,6 +375,7 @@ def main():
     from paper_1510_05041_b200.engine import get_engine
     lib = NN.load()
     NN.require_gpu()
+    f32 = cfg.get("dtype") == "f32"
     eng = get_engine(list(range(args.gpus)), 4)
     if os.environ.get("BX_TRSM_LEAF"):
         NN.check(lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"])), "trsm leaf")
@@ -349,7 +401,12 @@ def main():
 
     flops = e2e["flops"]
     h2d_bw, p2p_bw = 53.0e9, 700e9      # measured (profiles/peaks_r01.json); P2P: nominal-measured
-    t_a = flops / (args.gpus * peak.value * 1e12)
+    peak_tf = peak.value
+    peak_src = ("measured live: register-only DMMA.8x8x4 loop (bx_fp64_peak_probe); "
+                "MEASURED_PEAKS.json has no FP64 entry")
+    if f32:
+        peak_tf, peak_src = tf32_peak_tflops()
+    t_a = flops / (args.gpus * peak_tf * 1e12)
     t_b = e2e["h2d"] / (h2d_bw * args.gpus) + e2e["p2p"] / (p2p_bw * args.gpus)
     prof = os.path.join(ROOT, "profiles", "ncu_dgemm_traffic_r01.json")
     traffic = None
@@ -360,13 +417,13 @@ def main():
             traffic = None
     kernel_tf = val["kernel_tflops"] if val else e2e["value"]
     out = {
-        "metric": METRIC,
+        "metric": METRIC if not f32 else "SGEMM TFLOP/s (host-resident operands, tcgen05 kind::tf32), % of TF32 tensor peak",
         "value": val["value"] if val else e2e["value"],
         "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": val["ms_per_step"] if val else e2e["ms"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f32 (tf32 MMA, f32 accumulate)" if f32 else "f64",
         "data": "synthetic: seeded uniform[-1,1) (reference build_call generator) for e2e; "
                 "device-filled uniform[-1,1) for the HBM-resident leg",
         "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
@@ -376,20 +433,22 @@ def main():
         "e2e": {"value": e2e["value"], "unit": "TFLOP/s", "ms_per_step": e2e["ms"],
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                 "p2p_bytes_per_step": e2e["p2p"],
-                "frac_of_fp64_peak": e2e["value"] / (args.gpus * peak.value),
+                "frac_of_tensor_peak": e2e["value"] / (args.gpus * peak_tf),
                 "cache": {"l1_hits": e2e["l1"], "l2_hits": e2e["l2"], "host_fetches": e2e["host"]},
                 "per_device": e2e["per_device"],
                 "roofline_north_star": {"t_tensor_s": t_a, "t_link_s": t_b,
                                         "frac": max(t_a, t_b) / (e2e["ms"] / 1e3),
                                         "h2d_gbs_assumed": h2d_bw / 1e9, "p2p_gbs_assumed": p2p_bw / 1e9}},
-        "roofline": {"bound": "tensor", "achieved": kernel_tf, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": kernel_tf / peak.value, "traffic": traffic,
-                     "kernel": "bx::gemm_task_kernel (FP64 DMMA m8n8k4)",
-                     "peak_source": "measured live: register-only DMMA.8x8x4 loop (bx_fp64_peak_probe); "
-                                    "MEASURED_PEAKS.json has no FP64 entry",
+        "roofline": {"bound": "tensor", "achieved": kernel_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": kernel_tf / peak_tf, "traffic": None if f32 else traffic,
+                     "kernel": ("bx::sgemm_tc_kernel (tcgen05.mma kind::tf32, TMEM accumulators, TMA)"
+                                if f32 else "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
+                     "peak_source": peak_src,
+                     "fp64_dmma_peak_measured": peak.value,
                      "flops_per_launch": val["flops_per_launch"] if val else None,
                      "avg_launch_ms": val["avg_launch_ms"] if val else None},
         "gpu_launches": e2e["launches"] + (val["launches"] if val else 0),
+        **({"tile_sweep": e2e["sweep"]} if e2e["sweep"] else {}),
         "gpu_launches_e2e": e2e["launches"],
         "clocks": clk.summary(),
     }

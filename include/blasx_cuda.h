@@ -115,6 +115,7 @@ int bx_launch_count(uint64_t* n); /* kernels launched by this library since load
 int bx_dev_alloc(int dev, uint64_t bytes, uint64_t* ptr);
 int bx_dev_free(int dev, uint64_t ptr);
 int bx_dev_fill_uniform(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int stream);
+int bx_dev_fill_uniform_f32(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int stream);
 int bx_dev_copy_h2d(int dev, uint64_t dst, const void* src, uint64_t bytes);
 int bx_dev_copy_d2h(int dev, void* dst, uint64_t src, uint64_t bytes);
 int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, double alpha,

@@ -66,6 +66,7 @@ _SIGS = {
     "bx_dev_alloc": [_i, _u64, _pu64],
     "bx_dev_free": [_i, _u64],
     "bx_dev_fill_uniform": [_i, _u64, _u64, _u64, _i],
+    "bx_dev_fill_uniform_f32": [_i, _u64, _u64, _u64, _i],
     "bx_dev_copy_h2d": [_i, _u64, _p, _u64],
     "bx_dev_copy_d2h": [_i, _p, _u64, _u64],
     "bx_dgemm_device": [_i, _i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _d, _u64, _i],

@@ -430,6 +430,18 @@ int trsm_rec(cudaStream_t s, int right, int eff_upper, int trans, int unit, int 
   return trsm_rec(s, 1, 0, trans, unit, h, n1, 1.0, e11, lda, b1, ldb, flag, leaf_max);
 }
 
+__global__ void fill_uniform_f32_kernel(float* p, uint64_t n, uint64_t seed) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    p[i] = (float)((double)(z >> 40) * (2.0 / 16777216.0) - 1.0);
+  }
+}
+
 __global__ void fill_uniform_kernel(double* p, uint64_t n, uint64_t seed) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -882,6 +894,18 @@ int bx_dev_fill_uniform(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int st
   if (!s) return set_err(BX_EINVAL, "bad stream");
   CUDA_TRY(cudaSetDevice(D->cuda_id));
   fill_uniform_kernel<<<D->sms * 8, 256, 0, s>>>((double*)ptr, n, seed);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
+int bx_dev_fill_uniform_f32(int dev, uint64_t ptr, uint64_t n, uint64_t seed, int stream) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s) return set_err(BX_EINVAL, "bad stream");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  fill_uniform_f32_kernel<<<D->sms * 8, 256, 0, s>>>((float*)ptr, n, seed);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return BX_OK;

@@ -103,8 +103,16 @@ __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_con
   uint32_t* tmem_slot = (uint32_t*)(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_m = (t.h + S_BM - 1) / S_BM;
-  const int m0 = (blockIdx.x % tiles_m) * S_BM, n0 = (blockIdx.x / tiles_m) * S_BN;
+  // grouped rasterisation: consecutive CTAs sweep GROUP_M m-tiles before moving along n,
+  // so the CTAs in flight share A and B panels in L2 instead of streaming all of A per
+  // column of tiles (22x DRAM re-reads without it)
+  constexpr int GROUP_M = 8;
+  const int tiles_m = (t.h + S_BM - 1) / S_BM, tiles_n = (t.w + S_BN - 1) / S_BN;
+  const int per_group = GROUP_M * tiles_n;
+  const int first_m = (blockIdx.x / per_group) * GROUP_M;
+  const int gsize = min(tiles_m - first_m, GROUP_M);
+  const int m0 = (first_m + (blockIdx.x % per_group) % gsize) * S_BM;
+  const int n0 = ((blockIdx.x % per_group) / gsize) * S_BN;
 
   int total = 0;
   for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + S_BK - 1) / S_BK;

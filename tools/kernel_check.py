@@ -257,6 +257,18 @@ if "--launch-overhead" in sys.argv:
         lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
         print(f"{label}: host {(t1 - t0) / 50 * 1e6:.1f} us/call, gpu {ms.value / 50 * 1e3:.1f} us/launch")
 
+if "--sgemm-only-perf" in sys.argv:
+    for n in (16384,):
+        ptrs = []
+        for _ in range(3):
+            p = C.c_uint64()
+            N.check(lib.bx_dev_alloc(0, n * n * 4, C.byref(p)))
+            N.check(lib.bx_dev_fill_uniform_f32(0, p.value, n * n, 5, 0))
+            ptrs.append(p.value)
+        for _ in range(2):
+            N.check(lib.bx_sgemm_device(0, 0, 0, 0, n, n, n, 1.0, ptrs[0], n, ptrs[1], n, 0.0, ptrs[2], n))
+        lib.bx_device_sync(0)
+
 if "--sgemm" in sys.argv:
     def put32(arr):
         arr = np.asfortranarray(arr, dtype=np.float32)
@@ -305,11 +317,12 @@ if "--sgemm" in sys.argv:
                         print("FAIL sgemm", h, w, d, ns, ta, tb, beta, err, np.abs(out - ref).max())
     print("sgemm fails:", sf)
     if "--perf" in sys.argv or "--sgemm-perf" in sys.argv:
-        for n in (8192, 16384):
+        for n in (8192, 16384, 32768):
             ptrs = []
             for _ in range(3):
                 p = C.c_uint64()
                 N.check(lib.bx_dev_alloc(0, n * n * 4, C.byref(p)))
+                N.check(lib.bx_dev_fill_uniform_f32(0, p.value, n * n, 9, 0))
                 ptrs.append(p.value)
             for tt in [(0, 0), (0, 1), (1, 0), (1, 1)]:
                 N.check(lib.bx_sgemm_device(0, 0, tt[0], tt[1], n, n, n, 1.0, ptrs[0], n, ptrs[1], n, 0.0, ptrs[2], n))
