@@ -84,8 +84,13 @@ int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
     idx = fl.back();
     fl.pop_back();
   } else {
+    // events belong to the device current at creation: create on this slot's device
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != D->cuda_id) cudaSetDevice(D->cuda_id);
     cudaEvent_t e;
     cudaError_t err = cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+    if (cur != D->cuda_id && cur >= 0) cudaSetDevice(cur);
     if (err != cudaSuccess) return set_err(BX_ECUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(err));
     idx = (int)D->events.size();
     if (idx >= (1 << kEvShift)) return set_err(BX_ENOMEM, "event pool exhausted");
@@ -558,7 +563,7 @@ int bx_init(int ndev, const int* device_ids, const uint64_t* arena_bytes, int n_
   }
   for (int a = 0; a < ndev; ++a)
     for (int b = 0; b < ndev; ++b) {
-      if (a == b) continue;
+      if (a == b || g_devs[a].cuda_id == g_devs[b].cuda_id) continue;   // same GPU: no peer link
       int can = 0;
       CUDA_TRY(cudaDeviceCanAccessPeer(&can, g_devs[a].cuda_id, g_devs[b].cuda_id));
       if (!can) continue;

@@ -28,6 +28,7 @@ class DeviceDesc:
     speed: float = 37.1e12         # measured FP64 DMMA peak (informational)
     arena_capacity: int = 0        # bytes; 0 = auto
     peer_group: object = None
+    cuda_ordinal: Optional[int] = None   # GPU backing this device (default: device_id)
 
 
 @dataclass

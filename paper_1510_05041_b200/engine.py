@@ -19,10 +19,14 @@ LANE_H2D, LANE_D2H, LANE_P2P = N.LANE_H2D, N.LANE_D2H, N.LANE_P2P
 class CudaEngine:
     kind = "cuda"
 
-    def __init__(self, cuda_ids, n_compute: int = 4):
+    def __init__(self, cuda_ids, n_compute: int = 4, logical_ids=None):
         self.lib = N.load()
         N.require_gpu()
         self.cuda_ids = list(cuda_ids)
+        # logical device ids (DeviceDesc.device_id) -> engine slot; normally the CUDA
+        # ordinal itself, but several logical devices may share one GPU (multi-device
+        # tests on a single B200: each slot has its own streams, events and arena)
+        self.ids = list(logical_ids) if logical_ids is not None else list(cuda_ids)
         self.n_compute = n_compute
         self._arena = [0] * len(self.cuda_ids)
         self._lock = threading.Lock()
@@ -31,15 +35,18 @@ class CudaEngine:
 
     # ---- devices / memory -------------------------------------------------------------
 
-    def slot(self, cuda_id: int) -> int:
-        return self.cuda_ids.index(cuda_id)
+    def slot(self, device_id: int) -> int:
+        return self.ids.index(device_id)
 
-    def extend(self, more_ids, n_compute) -> None:
-        ids = self.cuda_ids + [d for d in more_ids if d not in self.cuda_ids]
+    def extend(self, more, n_compute) -> None:
+        """Add (logical id, cuda ordinal) pairs."""
+        new = [(i, c) for i, c in more if i not in self.ids]
+        ids = self.ids + [i for i, _ in new]
+        cuda = self.cuda_ids + [c for _, c in new]
         n_compute = max(n_compute, self.n_compute)
-        N.check(self.lib.bx_init(len(ids), N.int_array(ids), None, n_compute), "bx_init")
-        self._arena += [0] * (len(ids) - len(self.cuda_ids))
-        self.cuda_ids, self.n_compute = ids, n_compute
+        N.check(self.lib.bx_init(len(cuda), N.int_array(cuda), None, n_compute), "bx_init")
+        self._arena += [0] * len(new)
+        self.ids, self.cuda_ids, self.n_compute = ids, cuda, n_compute
 
     @property
     def ndev(self) -> int:
@@ -210,15 +217,20 @@ _ENGINE = None
 _ELOCK = threading.Lock()
 
 
-def get_engine(cuda_ids, n_compute=4) -> CudaEngine:
-    """The process-wide engine, extended to cover ``cuda_ids``.  Engine slots are
-    positions in its device list; use ``engine.slot(cuda_id)``."""
+def get_engine(device_ids, n_compute=4, cuda_ordinals=None) -> CudaEngine:
+    """The process-wide engine, extended to cover ``device_ids`` (logical ids; their CUDA
+    ordinals default to the ids themselves).  Use ``engine.slot(device_id)``."""
     global _ENGINE
+    device_ids = list(device_ids)
+    cuda = list(cuda_ordinals) if cuda_ordinals is not None else list(device_ids)
     with _ELOCK:
         if _ENGINE is None:
-            _ENGINE = CudaEngine(list(cuda_ids), n_compute)
+            _ENGINE = CudaEngine(cuda, n_compute, logical_ids=device_ids)
             return _ENGINE
-        missing = [d for d in cuda_ids if d not in _ENGINE.cuda_ids]
+        for i, c in zip(device_ids, cuda):
+            if i in _ENGINE.ids and _ENGINE.cuda_ids[_ENGINE.ids.index(i)] != c:
+                raise ValueError(f"logical device {i} is already bound to another GPU")
+        missing = [(i, c) for i, c in zip(device_ids, cuda) if i not in _ENGINE.ids]
         if missing or n_compute > _ENGINE.n_compute:
             _ENGINE.extend(missing, n_compute)
         return _ENGINE

@@ -779,7 +779,8 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     topology = topology or discover_topology()
     devs = topology.accelerators()
     if engine is None:
-        engine = get_engine([d.device_id for d in devs], options.n_streams)
+        engine = get_engine([d.device_id for d in devs], options.n_streams,
+                            [d.device_id if d.cuda_ordinal is None else d.cuda_ordinal for d in devs])
     esz = plan.dtype.itemsize
     per_tile = device_ld(plan.tile_size) * plan.tile_size * esz
     caps = {}

@@ -236,3 +236,52 @@ def test_cblas_sgemm():
     sgemm("N", "N", m, n, k, 1.0, a, m, b, k, 0.0, c, m, tile_size=256)
     ref = a.astype(np.float64) @ b.astype(np.float64)
     assert np.linalg.norm(c - ref) / np.linalg.norm(ref) < 1e-3
+
+
+VIRTUAL = [100, 101, 102]   # logical devices sharing GPU 0 (own streams, events, arenas)
+
+
+def _virtual_topo(n=3, arena=0):
+    return Topology([DeviceDesc(VIRTUAL[i], cuda_ordinal=0, peer_group="nvlink",
+                                arena_capacity=arena) for i in range(n)])
+
+
+@pytest.mark.parametrize("kind,kw", [
+    ("gemm", dict(beta=1.0)),
+    ("gemm", dict(trans_a=True, beta=0.0)),
+    ("syr2k", dict(uplo="lower", beta=1.0)),
+    ("trsm", dict(uplo="lower", side="left")),
+    ("trmm", dict(uplo="upper", side="right", trans_a=True)),
+])
+@pytest.mark.parametrize("execution", ["deterministic", "concurrent"])
+def test_multi_device_runtime_on_one_gpu(kind, kw, execution):
+    """The multi-GPU path (L2 peer copies, directory, stealing, per-device engines) on three
+    logical devices backed by one B200."""
+    n, k, t = 1536, 1024, 256
+    call = build_call(kind, m=n, n=n, k=k, tile_size=t, seed=21, trsm_scaled=True, **kw)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    res = run_call(call, _virtual_topo(), RunOptions(execution=execution))
+    p = dict(kw)
+    alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
+    ref = c0.copy()
+    tiled.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
+    kk = k if kind in ("gemm", "syrk", "syr2k") else n
+    assert _ratio(kind, call.c.matrix.as_2d(), ref, a, b, c0, alpha, beta, kk) <= tolerance.BOUND
+    m = res.metrics
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    assert m.total_d2d_bytes() == sum(d.d2d_out_bytes for d in m.devices.values())
+    if kind == "gemm":
+        assert m.l2_hits > 0 and len([v for v in res.tasks_by_device.values() if v]) > 1
+
+
+def test_multi_device_small_arenas_evict_on_one_gpu():
+    call = build_call("gemm", m=1024, n=1024, k=2048, tile_size=256, seed=22, beta=1.0)
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    tile = 256 * 256 * 8
+    res = run_call(call, _virtual_topo(2, arena=40 * tile), RunOptions(chunk_steps=2))
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=256, alpha=1.0, beta=1.0)
+    assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 2048) <= 10
