@@ -70,3 +70,22 @@ for frac in (0.1, 0.25, 0.5, 0.75, 1.0):
     hb = sum(1 for s, e in hs if e <= tq)
     kb = sum(1 for s, e in ks if e <= tq)
     print(f"t={tq*1e3:7.1f} ms  H2D done {hb}/{len(hs)}  kernels done {kb}/{len(ks)}")
+# utilisation over time: fraction of 1 ms bins where >= 3 kernels run
+import math
+end = ks[-1][1]
+bins = int(math.ceil(end * 1e3))
+occ = [0.0] * bins
+for s0, e0 in ks:
+    b0, b1 = int(s0 * 1e3), int(e0 * 1e3)
+    for b in range(b0, min(b1 + 1, bins)):
+        lo, hi = max(s0, b / 1e3), min(e0, (b + 1) / 1e3)
+        if hi > lo:
+            occ[b] += (hi - lo) * 1e3
+print("kernel-streams busy per 5 ms window:", [round(sum(occ[i:i + 5]) / 5, 1) for i in range(0, bins, 5)])
+h2d_bins = [0.0] * bins
+for s0, e0 in hs:
+    for b in range(int(s0 * 1e3), min(int(e0 * 1e3) + 1, bins)):
+        lo, hi = max(s0, b / 1e3), min(e0, (b + 1) / 1e3)
+        if hi > lo:
+            h2d_bins[b] += (hi - lo) * 1e3
+print("H2D busy fraction per 5 ms window:", [round(sum(h2d_bins[i:i + 5]) / 5, 2) for i in range(0, bins, 5)])
