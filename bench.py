@@ -299,7 +299,8 @@ def e2e_leg(args, cfg, eng):
     from paper_1510_05041_b200.devices import DeviceDesc, Topology
     call = make_operands(cfg, seed=0)
     topo = Topology([DeviceDesc(g, peer_group="nvlink") for g in range(args.gpus)])
-    opts = RunOptions(chunk_steps=args.chunk)
+    opts = RunOptions(chunk_steps=args.chunk, n_streams=args.streams,
+                      tasks_per_stream=args.tasks_per_stream)
     for m in (call.a, call.b, call.c):
         if m is not None:
             eng.register_host(m.matrix.storage)   # page-locking excluded from timing
@@ -352,6 +353,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--chunk", type=int, default=16)
+    ap.add_argument("--streams", type=int, default=0)
+    ap.add_argument("--tasks-per-stream", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -76,7 +76,7 @@ class RunOptions:
     l1_enabled: bool = True
     l2_enabled: bool = True
     record_trace: bool = False
-    n_streams: int = 4
+    n_streams: int = 0                 # compute streams per GPU; 0 = auto (4, TRSM 8)
     chunk_steps: int = 16              # k-steps fused per kernel launch
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
     first_chunk_steps: int = 4         # shorter first launch per task (ramp-up); 0 = off
@@ -768,6 +768,11 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     from .engine import get_engine
     t_setup0 = time.perf_counter()
     options = options or RunOptions()
+    if not options.n_streams:
+        # 4 streams (the reference's lanes, devices.py:36); TRSM gets 8 because its
+        # diagonal solves are latency-bound and leave SMs idle unless more tasks overlap
+        import dataclasses
+        options = dataclasses.replace(options, n_streams=8 if plan.call.kind == "trsm" else 4)
     if options.execution not in ("deterministic", "concurrent"):
         raise ConfigError(f"unknown execution mode {options.execution!r}")
     if not 1 <= options.n_streams <= 8:

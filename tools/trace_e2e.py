@@ -14,9 +14,13 @@ t = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 tps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 fc = int(sys.argv[5]) if len(sys.argv) > 5 else 4
-call = build_call("gemm", m=n, n=n, k=n, tile_size=t, seed=0, alpha=1.0, beta=1.0)
+import os
+kind = os.environ.get("BX_KIND", "gemm")
+call = build_call(kind, m=n, n=n, k=n, tile_size=t, seed=0, alpha=1.0,
+                  beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0, uplo="lower",
+                  trsm_scaled=True)
 eng = get_engine([0])
-for x in (call.a, call.b, call.c):
+for x in [y for y in (call.a, call.b, call.c) if y is not None]:
     eng.register_host(x.matrix.storage)
 kw = dict(chunk_steps=chunk, tasks_per_stream=tps, first_chunk_steps=fc)
 run_call(call, options=RunOptions(**kw))
