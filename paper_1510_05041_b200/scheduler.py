@@ -202,7 +202,8 @@ class _Runtime:
 class _Active:
     """A task in flight on one compute stream."""
     __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
-                 "events", "last_ev", "done_ev", "pending_waits", "flops")
+                 "events", "last_ev", "done_ev", "pending_waits", "flops", "prog", "res",
+                 "next_op", "lazy", "misses", "misses_epoch")
 
     def __init__(self, entry, stream):
         self.entry = entry
@@ -391,16 +392,19 @@ class _GpuWorker:
         return self.rs.pop_best()
 
     def fill(self) -> bool:
-        issued = False
+        fresh = []
         for s, act in enumerate(self.active):
             if act is not None:
                 continue
             entry = self._next_entry()
             if entry is None:
                 break
-            self._issue(entry, s)
-            issued = True
-        return issued
+            fresh.append(self._begin(entry, s))
+        # one launch group per fresh task per round (k-major fetch order across them)
+        pending = fresh
+        while pending:
+            pending = [a for a in pending if not self._advance(a)]
+        return bool(fresh)
 
     # ---- issue ----------------------------------------------------------------------
 
@@ -455,14 +459,18 @@ class _GpuWorker:
             f"device {self.device_id}: one launch's tiles cannot all fit in the arena at once; "
             f"enlarge the arena or shrink the tiles")
 
-    def _resolve_resident(self, task):
+    def _resolve_resident(self, task, subset=None):
         """Resident mode: the arena was sized to hold every input tile of the call, so the
         ALRU can never evict.  Each block is pinned once, permanently, when it arrives, and
-        a task's translation reduces to lookups (no per-task pins / recency updates)."""
+        a task's translation reduces to lookups (no per-task pins / recency updates).
+        ``subset`` restricts the work to some of the task's tiles (one launch group)."""
         cache = self.cache
         blocks = cache._blocks
         keys = task_keys(task)
         ks = task._bx_keyset
+        if subset is not None:
+            ks = subset
+            keys = {k: keys[k] for k in subset}
         pend = self._pending_keys
         if pend and not pend.isdisjoint(ks):
             # drop keys whose copies have landed
@@ -475,7 +483,7 @@ class _GpuWorker:
                     pend.discard(k)
         if ks <= blocks.keys() and pend.isdisjoint(ks):
             # steady state: every tile resident and landed
-            self.l1_hits += task._bx_refs
+            self.l1_hits += task._bx_refs if subset is None else sum(m for _, m in keys.values())
             return {k: (b.offset, b.ld, None) for k in ks for b in (blocks[k],)}
         out = {}
         eng = self.eng
@@ -578,15 +586,13 @@ class _GpuWorker:
         act.pins = []
         self.dm.kernel_launches += 1
 
-    def _issue(self, entry, stream) -> None:
+    def _begin(self, entry, slot_index):
+        """Issue a task's C buffer (and C move-in) and compile its launch program; the
+        launches themselves are enqueued by ``_advance`` one launch group at a time."""
         task = entry.task
-        call = self.plan.call
         opts = self.runtime.options
-        slot_index = stream
-        stream = stream % self.n_streams
-        act = _Active(entry, stream)
+        act = _Active(entry, slot_index % self.n_streams)
         self._cur = act
-        eng, slot = self.eng, self.slot
         try:
             out = task.out_ref
             h, w = out.phys_height, out.phys_width
@@ -594,40 +600,79 @@ class _GpuWorker:
             act.c_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
             if task.needs_c_move_in:
                 desc, r0, c0 = self._host_of(out)
-                ev = self._timed(LANE_H2D, lambda wt: eng.h2d(
-                    slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
+                ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(
+                    self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
                     h * w * self.esz)
                 act.events.append(ev)
                 act.pending_waits.append(ev)
                 self.dm.h2d_bytes += h * w * self.esz
-            prog = compile_task(task, call, self.chunk_steps, opts.first_chunk_steps)
-            lazy = opts.l1_enabled and not self.resident
-            self._task_misses = 0
+            act.prog = compile_task(task, self.plan.call, self.chunk_steps, opts.first_chunk_steps)
+            act.lazy = opts.l1_enabled and not self.resident
+            act.misses = 0
+            act.misses_epoch = self._sync_epoch
             if not opts.l1_enabled:
-                res = self._resolve_uncached(task)
-            elif self.resident:
-                res = self._resolve_resident(task)
+                act.res = self._resolve_uncached(task)
             else:
-                res = {}
-            for i, n in enumerate(prog.scratch_n):
+                act.res = {}
+            for i, n in enumerate(act.prog.scratch_n):
                 ld = device_ld(n)
                 off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
                 act.scratch.append(off)
-                res[scratch_key(i)] = (off, ld, None)
-            for op in prog.ops:
-                if lazy:
-                    res = self._resolve_op(task, op, res)
+                act.res[scratch_key(i)] = (off, ld, None)
+            act.next_op = 0
+            act.flops = task.flops
+        finally:
+            self._cur = None
+        self.active[slot_index] = act
+        return act
+
+    def _advance(self, act) -> bool:
+        """Enqueue the task's next launch group (its tile fetches, then the launch); after
+        the last group, enqueue the write-back.  Returns True once the task is fully
+        issued.  Interleaving groups across freshly issued tasks orders the H2D queue
+        k-major across them, so they share panel tiles early instead of one task
+        fetching its whole k-range first."""
+        task = act.entry.task
+        call = self.plan.call
+        opts = self.runtime.options
+        ops = act.prog.ops
+        eng, slot, stream = self.eng, self.slot, act.stream
+        out = task.out_ref
+        h, w = out.phys_height, out.phys_width
+        self._cur = act
+        self._task_misses = act.misses
+        try:
+            res = act.res
+            i = act.next_op
+            while i < len(ops):
+                op = ops[i]
+                i += 1
+                if act.lazy:
+                    if act.misses_epoch != self._sync_epoch:
+                        # a pressure sync released this task's earlier pins: forget them
+                        for k in [k for k in res if k[0] != "#scratch"]:
+                            del res[k]
+                        act.misses_epoch = self._sync_epoch
+                    res = act.res = self._resolve_op(task, op, res)
+                    act.misses_epoch = self._sync_epoch
+                elif opts.l1_enabled:
+                    want = ({k for ak, bk, _ in op.subs for k in (ak, bk) if k[0] != "#scratch"}
+                            if type(op) is GemmOp else {op.key})
+                    want -= res.keys()
+                    if want:
+                        res.update(self._resolve_resident(task, frozenset(want)))
                 if type(op) is GemmOp:
                     ops_ = [(res[ak], res[bk], d) for ak, bk, d in op.subs]
-                    steps = [(a[0], a[1], b[0], b[1], d) for a, b, d in ops_]
+                    steps = [(a_[0], a_[1], b_[0], b_[1], d) for a_, b_, d in ops_]
                     waits = list(dict.fromkeys(
-                        w_ for a, b, _ in ops_ for w_ in (a[2], b[2]) if w_ is not None))
+                        w_ for a_, b_, _ in ops_ for w_ in (a_[2], b_[2]) if w_ is not None))
                     waits += act.pending_waits
                     act.pending_waits = []
                     ev = self._timed(stream, lambda wt, op=op, steps=steps: eng.gemm(
                         slot, stream, op.ta, op.tb, op.tri, h, w, steps, op.alpha, op.beta,
                         act.c_off, act.c_ld, wt, f32=self.f32), waits, "KERNEL", op.flops, op.k)
                     self._launched(act, ev)
+                    break
                 elif type(op) is MatOp:
                     ao, al, aw = res[op.key]
                     so, sl, _ = res[scratch_key(op.scratch)]
@@ -645,6 +690,11 @@ class _GpuWorker:
                         call.diag == "unit", h, w, op.alpha, ao, al, act.c_off, act.c_ld, wt),
                         waits, "KERNEL", op.flops, op.k)
                     self._launched(act, ev)
+                    break
+            act.next_op = i
+            act.misses = self._task_misses
+            if i < len(ops):
+                return False
             desc, r0, c0 = self._host_of(out)
             waits = [act.last_ev] + act.pending_waits
             act.pending_waits = []
@@ -653,12 +703,12 @@ class _GpuWorker:
                 h * w * self.esz)
             self.dm.d2h_bytes += h * w * self.esz
             act.events.append(act.done_ev)
-            act.flops = task.flops
-            if lazy:
-                self.l1_hits += task._bx_refs - self._task_misses
+            if act.lazy:
+                self.l1_hits += task._bx_refs - act.misses
+            act.res = None
+            return True
         finally:
             self._cur = None
-        self.active[slot_index] = act
 
     # ---- completion -----------------------------------------------------------------
 
@@ -699,7 +749,7 @@ class _GpuWorker:
     def _retire_finished(self, block: bool) -> bool:
         got = False
         for s, act in enumerate(self.active):
-            if act is None:
+            if act is None or act.done_ev is None:
                 continue
             if self.eng.done(act.done_ev):
                 self.active[s] = None
