@@ -125,6 +125,8 @@ int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 d
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 128); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);
+/* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile */
+int bx_set_sgemm_variant(int variant);
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha,
                     uint64_t a, int lda, uint64_t b, int ldb, float beta, uint64_t c, int ldc);
 /* register-only DMMA loop: measured FP64 tensor peak for the roofline denominator */

@@ -263,6 +263,8 @@ int tensor_map_f32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
   return BX_OK;
 }
 
+int g_sgemm_variant = 0;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile
+
 // fp32 task GEMM on tcgen05 (TF32 inputs, fp32 accumulation in TMEM)
 int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
               const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c, int ldc) {
@@ -289,10 +291,22 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
       if (!ta) rc = tensor_map_f32(a[j], h, d, lda[j], 32, 32, MN, &t.steps[i].map_a);
       else rc = tensor_map_f32(a[j], d, h, lda[j], bx::S_BK, bx::S_BM, KM, &t.steps[i].map_a);
       if (rc) return rc;
-      // B: untransposed K x N (K-major box 32 x 256), transposed N x K (MN-major boxes 32x32)
-      if (!tb) rc = tensor_map_f32(b[j], d, w, ldb[j], bx::S_BK, bx::S_BN, KM, &t.steps[i].map_b);
+      // B: untransposed K x N (K-major box 32 x BN per CTA), transposed N x K (MN boxes 32x32)
+      const uint32_t bn_box = g_sgemm_variant == 1 ? 128u : (uint32_t)bx::S_BN;
+      if (!tb) rc = tensor_map_f32(b[j], d, w, ldb[j], bx::S_BK, bn_box, KM, &t.steps[i].map_b);
       else rc = tensor_map_f32(b[j], w, d, ldb[j], 32, 32, MN, &t.steps[i].map_b);
       if (rc) return rc;
+    }
+    if (g_sgemm_variant == 1) {
+      if (need_attr((const void*)bx::sgemm_tc2_kernel)) {
+        CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::P_SMEM_BYTES));
+      }
+      int pairs = ((h + bx::P_BM - 1) / bx::P_BM) * ((w + bx::P_BN - 1) / bx::P_BN);
+      bx::sgemm_tc2_kernel<<<2 * pairs, bx::P_THREADS, bx::P_SMEM_BYTES, s>>>(t);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+      if (nsteps <= 0) break;
+      continue;
     }
     if (need_attr((const void*)bx::sgemm_tc_kernel)) {
       CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::S_SMEM_BYTES));
@@ -946,6 +960,12 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
 
 int bx_set_gemm_variant(int v) {
   g_gemm_variant = v;
+  return BX_OK;
+}
+
+int bx_set_sgemm_variant(int v) {
+  if (v < 0 || v > 1) return set_err(BX_EINVAL, "sgemm variant must be 0 or 1");
+  g_sgemm_variant = v;
   return BX_OK;
 }
 

@@ -235,3 +235,181 @@ __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_con
 }
 
 }  // namespace bx
+
+// ---------------------------------------------------------------------------------------
+// 2-SM variant: a cluster of two CTAs (one TPC) runs tcgen05.mma.cta_group::2 with
+// M = 256 (each CTA owns 128 rows of A and of the accumulator) and N = 256 (each CTA
+// stages 128 columns of B; the MMA reads both halves).  Per pair and k-slab 64 KB are
+// loaded for 256x256x32 MACs — 1.5x less L2 traffic per flop than the 1-SM 128x256 tile,
+// which ran out of L2 bandwidth.  Both CTAs' TMA loads complete on the leader's "full"
+// barrier (peer bit cleared from the cluster address); the leader's commit multicasts to
+// both CTAs' "empty" and "accum" barriers.
+// ---------------------------------------------------------------------------------------
+namespace bx {
+
+constexpr int P_BM = 256, P_BN = 256, P_BK = 32, P_STAGES = 6, P_THREADS = 192;
+constexpr int P_A_BYTES = 128 * P_BK * 4;                 // this CTA's 128 rows of A
+constexpr int P_B_BYTES = 128 * P_BK * 4;                 // this CTA's 128 columns of B
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;      // 32 KB
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;               // leader CTA's copy of a smem address
+
+__device__ __forceinline__ uint32_t p_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void p_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void p_mbar_wait(uint64_t* b, uint32_t parity) {
+  // bounded spin during bring-up: trap instead of hanging the GPU on a protocol bug
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .u32 n;\n mov.u32 n, 0;\n W_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @p bra D_%=;\n add.u32 n, n, 1;\n setp.gt.u32 p, n, 200000000;\n @p trap;\n bra W_%=;\n D_%=:\n}\n"
+      ::"r"(s_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void p_tma_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar) & PEER_MASK), "r"(c0), "r"(c1) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
+    sgemm_tc2_kernel(const __grid_constant__ SgemmTask t) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)s_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* accum = empty + P_STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = p_cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  constexpr int GROUP_M = 4;
+  const int tiles_m = (t.h + P_BM - 1) / P_BM, tiles_n = (t.w + P_BN - 1) / P_BN;
+  const int per_group = GROUP_M * tiles_n;
+  const int first_m = (pair / per_group) * GROUP_M;
+  const int gsize = min(tiles_m - first_m, GROUP_M);
+  const int m0 = (first_m + (pair % per_group) % gsize) * P_BM;
+  const int n0 = ((pair % per_group) / gsize) * P_BN;
+  const int my_m0 = m0 + 128 * (int)rank;   // rows of A / accumulator held by this CTA
+  const int my_n0 = n0 + 128 * (int)rank;   // columns of B staged by this CTA
+
+  int total = 0;
+  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + P_BK - 1) / P_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) { s_mbar_init(&full[s], 1); s_mbar_init(&empty[s], 1); }
+    s_mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(tmem_slot)), "n"(S_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  s_fence_before();
+  p_cluster_sync();
+  s_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int step = 0, k0 = 0;
+      for (int it = 0; it < total; ++it) {
+        const int st = it % P_STAGES;
+        if (it >= P_STAGES) p_mbar_wait(&empty[st], ((it / P_STAGES) - 1) & 1);
+        uint8_t* sa = smem + st * P_STAGE_BYTES;
+        uint8_t* sb = sa + P_A_BYTES;
+        // the leader's barrier expects both CTAs' bytes
+        if (rank == 0) s_mbar_expect_tx(&full[st], 2 * P_STAGE_BYTES);
+        const CUtensorMap* ma = &t.steps[step].map_a;
+        const CUtensorMap* mb = &t.steps[step].map_b;
+        if (t.ta) {
+          p_tma_2d_pair(sa, ma, &full[st], k0, my_m0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p_tma_2d_pair(sa + i * 4096, ma, &full[st], my_m0 + 32 * i, k0);
+        }
+        if (!t.tb) {
+          p_tma_2d_pair(sb, mb, &full[st], k0, my_n0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p_tma_2d_pair(sb + i * 4096, mb, &full[st], my_n0 + 32 * i, k0);
+        }
+        k0 += P_BK;
+        if (k0 >= t.steps[step].d) { k0 = 0; ++step; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      uint32_t idesc = s_idesc(!t.ta, t.tb);
+      idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(P_BM >> 4) << 24);   // M = 256
+      for (int it = 0; it < total; ++it) {
+        const int st = it % P_STAGES;
+        p_mbar_wait(&full[st], (it / P_STAGES) & 1);
+        s_fence_after();
+        const uint32_t sa = s_u32(smem + st * P_STAGE_BYTES);
+        const uint32_t sb = sa + P_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < P_BK / 8; ++kk) {
+          const uint64_t da = t.ta ? s_desc(sa + kk * 32, 16, 1024, 2) : s_desc(sa + kk * 1024, t.mn_lbo, t.mn_sbo, 1);
+          const uint64_t db = t.tb ? s_desc(sb + kk * 1024, t.mn_lbo, t.mn_sbo, 1) : s_desc(sb + kk * 32, 16, 1024, 2);
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                     ::"r"(s_u32(&empty[st])), "h"((uint16_t)3) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   ::"r"(s_u32(accum)), "h"((uint16_t)3) : "memory");
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = my_m0 + 32 * q + lane;
+    if (total > 0) {
+      p_mbar_wait(accum, 0);
+      s_fence_after();
+    }
+    for (int c0 = 0; c0 < P_BN; c0 += 16) {
+      uint32_t v[16];
+      if (total > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0u;
+      }
+      if (row < t.h) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = n0 + c0 + i;
+          if (col < t.w) {
+            float* p = t.c + (size_t)col * t.ldc + row;
+            float r = t.alpha * __uint_as_float(v[i]);
+            if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
+            *p = r;
+          }
+        }
+      }
+    }
+  }
+  s_fence_before();
+  p_cluster_sync();
+  if (warp == 1) {
+    s_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(S_TMEM_COLS));
+  }
+}
+
+}  // namespace bx

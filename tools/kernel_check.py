@@ -257,6 +257,10 @@ if "--launch-overhead" in sys.argv:
         lib.bx_event_elapsed(e0.value, e1.value, C.byref(ms))
         print(f"{label}: host {(t1 - t0) / 50 * 1e6:.1f} us/call, gpu {ms.value / 50 * 1e3:.1f} us/launch")
 
+for _a in sys.argv:
+    if _a.startswith("--sgemm-variant="):
+        N.check(lib.bx_set_sgemm_variant(int(_a.split("=")[1])))
+
 if "--sgemm-only-perf" in sys.argv:
     for n in (16384,):
         ptrs = []
