@@ -357,8 +357,11 @@ def main():
     ap.add_argument("--tasks-per-stream", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tile", type=int, default=0, help="override the config's tile size")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.tile:
+        cfg = dict(cfg, tile=args.tile, desc=cfg["desc"].replace(f"tile {cfg['tile']}", f"tile {args.tile}"))
     rank, world = dist_env()
     dist = maybe_init_dist()
 
