@@ -1,0 +1,56 @@
+/* TEST/TOOL STUB (never shipped): the libblasx_cuda.so ABI with every call a no-op that
+ * completes immediately.  tools/host_cost.py loads it in place of the real library to time
+ * the Python runtime + ctypes marshalling per task without a GPU. */
+#include <stdint.h>
+#include <string.h>
+static int ev_next = 0;
+static uint64_t launches = 0;
+#define EV(p) (*(p) = ev_next++, 0)
+int bx_version(void) { return 1; }
+int bx_device_count(int *n) { *n = 8; return 0; }
+int bx_device_info(int dev, char *name, int len, int *sms, uint64_t *tot, uint64_t *fr) {
+    strncpy(name, "stub", len); *sms = 148; *tot = 180ull << 30; *fr = 170ull << 30; return 0; }
+int bx_mem_info(int dev, uint64_t *fr, uint64_t *tot) { *fr = 170ull << 30; *tot = 180ull << 30; return 0; }
+int bx_init() { return 0; }
+int bx_shutdown() { return 0; }
+int bx_arena_base(int d, uint64_t *b) { *b = 0; return 0; }
+int bx_peer_enabled(int a, int b, int *e) { *e = 1; return 0; }
+int bx_host_register() { return 0; }
+int bx_host_unregister() { return 0; }
+int bx_host_is_registered(const void *p, int *yes) { *yes = 1; return 0; }
+int bx_h2d_tile(int d, uint64_t o, int ld, const void *s, int64_t sl, int h, int w, int e, int n, const int *wt, int *ev) { return EV(ev); }
+int bx_d2h_tile(int d, uint64_t o, int ld, void *s, int64_t sl, int h, int w, int e, int n, const int *wt, int *ev) { return EV(ev); }
+int bx_p2p_tile(int d, uint64_t o, int s, uint64_t so, uint64_t b, int n, const int *wt, int *ev) { return EV(ev); }
+int bx_gemm_task(int d, int s, int ta, int tb, int tri, int h, int w, int ns, const uint64_t *a, const int *la,
+                 const uint64_t *b, const int *lb, const int *dp, double al, double be, uint64_t c, int lc,
+                 int n, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_sgemm_task(int d, int s, int ta, int tb, int h, int w, int ns, const uint64_t *a, const int *la,
+                  const uint64_t *b, const int *lb, const int *dp, double al, double be, uint64_t c, int lc,
+                  int n, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_trsm_tile(int d, int s, int r, int u, int t, int un, int h, int w, double al, uint64_t a, int la,
+                 uint64_t b, int lb, int n, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_materialize(int d, int s, int m, int u, int t, int un, int n, uint64_t a, int la, uint64_t o, int lo,
+                   int nw, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_singular_flag(int d, int r, int *f) { *f = 0; return 0; }
+int bx_event_record(int d, int s, int t, int *ev) { return EV(ev); }
+int bx_event_query(int ev) { return 0; }
+int bx_event_sync() { return 0; }
+int bx_event_wait_any(int n, const int *evs, int *idx, int spin) { *idx = 0; return 0; }
+int bx_event_elapsed(int a, int b, float *ms) { *ms = 1.0f; return 0; }
+int bx_event_release() { return 0; }
+int bx_stream_wait() { return 0; }
+int bx_device_sync() { return 0; }
+int bx_launch_count(uint64_t *n) { *n = launches; return 0; }
+int bx_dev_alloc(int d, uint64_t b, uint64_t *p) { *p = 0; return 0; }
+int bx_dev_free() { return 0; }
+int bx_dev_fill_uniform() { return 0; }
+int bx_dev_fill_uniform_f32() { return 0; }
+int bx_dev_copy_h2d() { return 0; }
+int bx_dev_copy_d2h() { return 0; }
+int bx_dgemm_device() { return 0; }
+int bx_set_gemm_variant() { return 0; }
+int bx_set_trsm_leaf() { return 0; }
+int bx_set_sgemm_variant() { return 0; }
+int bx_sgemm_device() { return 0; }
+int bx_fp64_peak_probe(int d, int it, double *tf) { *tf = 37.0; return 0; }
+int bx_last_error(char *buf, int len) { if (len) buf[0] = 0; return 0; }
