@@ -134,6 +134,30 @@ int bx_fp64_peak_probe(int dev, int iters, double* tflops);
 
 int bx_last_error(char* buf, int len);
 
+/* ---- one process per GPU (spmd.py) ---------------------------------------------------
+ * The reference drives every device from one process (scheduler.py:597-663); on B200 the
+ * host side runs one process per GPU, so the L2 tile cache reaches peer arenas through
+ * CUDA IPC, tile arrival is signalled through device-written flags in node-shared pinned
+ * host memory (stream memory operations: a peer's copy waits on the flag on the GPU, no
+ * host round trip), and the shared scheduler state uses host atomics. */
+/* IPC handle (64 bytes) of this slot's arena, and the arena size */
+int bx_ipc_arena_handle(int dev, void* handle64, uint64_t* arena_bytes);
+/* open a peer process's arena in this slot's context; *base = its device address */
+int bx_ipc_open(int dev, const void* handle64, uint64_t* base);
+int bx_ipc_close(int dev, uint64_t base);
+/* page-lock + map host memory (flags); *dev_ptr = the address kernels / stream ops use */
+int bx_host_register_mapped(void* ptr, uint64_t bytes, uint64_t* dev_ptr);
+/* copy_from_peer across processes (replaces cache.py:312-322 for a remote holder): on the
+ * P2P lane, optionally wait until the 32-bit flag at flag_dptr >= flag_min, then copy
+ * `bytes` from the device address src_ptr (an IPC-opened peer arena) into this arena */
+int bx_copy_remote(int dst_dev, uint64_t dst_off, uint64_t src_ptr, uint64_t bytes, uint64_t flag_dptr,
+                   uint32_t flag_min, int n_wait, const int* wait, int* ev_out);
+/* on `lane`, after the waits, write `value` to the flag at flag_dptr (arrival signal) */
+int bx_write_flag(int dev, int lane, uint64_t flag_dptr, uint32_t value, int n_wait, const int* wait);
+/* host atomics on node-shared memory (64-bit, sequentially consistent) */
+int bx_atomic_add(int64_t* p, int64_t v, int64_t* old);
+int bx_atomic_cas(int64_t* p, int64_t expected, int64_t desired, int64_t* old);
+
 #ifdef __cplusplus
 }
 #endif

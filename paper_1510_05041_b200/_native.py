@@ -75,6 +75,14 @@ _SIGS = {
     "bx_set_trsm_leaf": [_i],
     "bx_set_sgemm_variant": [_i],
     "bx_last_error": [C.c_char_p, _i],
+    "bx_ipc_arena_handle": [_i, _p, _pu64],
+    "bx_ipc_open": [_i, _p, _pu64],
+    "bx_ipc_close": [_i, _u64],
+    "bx_host_register_mapped": [_p, _u64, _pu64],
+    "bx_copy_remote": [_i, _u64, _u64, _u64, _u64, C.c_uint32, _i, _pi, _pi],
+    "bx_write_flag": [_i, _i, _u64, C.c_uint32, _i, _pi],
+    "bx_atomic_add": [_p, C.c_int64, C.POINTER(C.c_int64)],
+    "bx_atomic_cas": [_p, C.c_int64, C.c_int64, C.POINTER(C.c_int64)],
 }
 
 

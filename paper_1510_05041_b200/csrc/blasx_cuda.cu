@@ -1001,4 +1001,119 @@ int bx_fp64_peak_probe(int dev, int iters, double* tflops) {
   return BX_OK;
 }
 
+// ---- one process per GPU: IPC arenas, device-visible flags, host atomics ---------------
+
+int bx_ipc_arena_handle(int dev, void* handle64, uint64_t* arena_bytes) {
+  Device* D = dev_of(dev);
+  if (!D || !D->arena) return set_err(BX_EINVAL, "ipc handle: no arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, D->arena));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle64, &h, sizeof(h));
+  *arena_bytes = D->arena_bytes;
+  return BX_OK;
+}
+
+int bx_ipc_open(int dev, const void* handle64, uint64_t* base) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = (uint64_t)p;
+  return BX_OK;
+}
+
+int bx_ipc_close(int dev, uint64_t base) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  CUDA_TRY(cudaIpcCloseMemHandle((void*)base));
+  return BX_OK;
+}
+
+int bx_host_register_mapped(void* ptr, uint64_t bytes, uint64_t* dev_ptr) {
+  if (!ptr || !bytes) return set_err(BX_EINVAL, "register: null");
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();
+  else if (e != cudaSuccess) { cudaGetLastError(); return set_err(BX_ECUDA, std::string("cudaHostRegister(mapped): ") + cudaGetErrorString(e)); }
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_registered[ptr] = bytes;
+  }
+  void* d = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(&d, ptr, 0));
+  *dev_ptr = (uint64_t)d;
+  return BX_OK;
+}
+
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32 g_wait32 = nullptr;
+PFN_writeValue32 g_write32 = nullptr;
+
+int stream_ops_init() {
+  if (g_wait32 && g_write32) return BX_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return set_err(BX_ECUDA, "cuStreamWaitValue32 unavailable");
+  g_wait32 = (PFN_waitValue32)fn;
+  fn = nullptr;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return set_err(BX_ECUDA, "cuStreamWriteValue32 unavailable");
+  g_write32 = (PFN_writeValue32)fn;
+  return BX_OK;
+}
+
+int bx_copy_remote(int dst_dev, uint64_t dst_off, uint64_t src_ptr, uint64_t bytes, uint64_t flag_dptr,
+                   uint32_t flag_min, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dst_dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  if (!src_ptr || dst_off + bytes > D->arena_bytes) return set_err(BX_EINVAL, "copy_remote: outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(D->p2p, n_wait, wait);
+  if (rc) return rc;
+  if (flag_dptr) {
+    rc = stream_ops_init();
+    if (rc) return rc;
+    CUresult r = g_wait32((CUstream)D->p2p, (CUdeviceptr)flag_dptr, flag_min, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return set_err(BX_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+  }
+  CUDA_TRY(cudaMemcpyAsync(D->arena + dst_off, (const void*)src_ptr, bytes, cudaMemcpyDeviceToDevice, D->p2p));
+  return finish(dst_dev, D->p2p, ev_out);
+}
+
+int bx_write_flag(int dev, int lane, uint64_t flag_dptr, uint32_t value, int n_wait, const int* wait) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, lane);
+  if (!s || !flag_dptr) return set_err(BX_EINVAL, "write_flag: bad lane / flag");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = stream_ops_init();
+  if (rc) return rc;
+  rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  CUresult r = g_write32((CUstream)s, (CUdeviceptr)flag_dptr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return set_err(BX_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+  return BX_OK;
+}
+
+int bx_atomic_add(int64_t* p, int64_t v, int64_t* old) {
+  if (!p || ((uintptr_t)p & 7)) return set_err(BX_EINVAL, "atomic_add: misaligned");
+  *old = __atomic_fetch_add(p, v, __ATOMIC_SEQ_CST);
+  return BX_OK;
+}
+
+int bx_atomic_cas(int64_t* p, int64_t expected, int64_t desired, int64_t* old) {
+  if (!p || ((uintptr_t)p & 7)) return set_err(BX_EINVAL, "atomic_cas: misaligned");
+  int64_t e = expected;
+  __atomic_compare_exchange_n(p, &e, desired, false, __ATOMIC_SEQ_CST, __ATOMIC_SEQ_CST);
+  *old = e;
+  return BX_OK;
+}
+
 }  // extern "C"

@@ -122,6 +122,42 @@ class CudaEngine:
                                      C.byref(ev)), "p2p tile")
         return ev.value
 
+    # ---- one process per GPU (spmd.py) ---------------------------------------------------
+
+    def ipc_export(self, slot):
+        """(64-byte IPC handle of the arena, arena bytes)."""
+        h = C.create_string_buffer(64)
+        n = C.c_uint64()
+        N.check(self.lib.bx_ipc_arena_handle(slot, h, C.byref(n)), "ipc handle")
+        return h.raw, n.value
+
+    def ipc_open(self, slot, handle: bytes) -> int:
+        base = C.c_uint64()
+        N.check(self.lib.bx_ipc_open(slot, C.create_string_buffer(handle, 64), C.byref(base)),
+                "ipc open")
+        return base.value
+
+    def ipc_close(self, slot, base) -> None:
+        N.check(self.lib.bx_ipc_close(slot, base), "ipc close")
+
+    def register_mapped(self, array) -> int:
+        """Page-lock + map a host buffer (device-written flags); returns its device address."""
+        d = C.c_uint64()
+        N.check(self.lib.bx_host_register_mapped(C.c_void_p(array.ctypes.data), array.nbytes,
+                                                 C.byref(d)), "register mapped")
+        return d.value
+
+    def copy_remote(self, slot, dst_off, src_ptr, nbytes, flag_dptr=0, flag_min=0, waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_copy_remote(slot, dst_off, src_ptr, nbytes, flag_dptr, flag_min, nw, wp,
+                                        C.byref(ev)), "copy remote")
+        return ev.value
+
+    def write_flag(self, slot, lane, flag_dptr, value, waits=()) -> None:
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_write_flag(slot, lane, flag_dptr, value, nw, wp), "write flag")
+
     # ---- kernels ------------------------------------------------------------------------
 
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),

@@ -71,7 +71,8 @@ class TaskQueue:
 
 @dataclass
 class RunOptions:
-    execution: str = "deterministic"   # one driver thread; "concurrent": one per GPU
+    execution: str = "deterministic"   # one driver thread; "concurrent": one per GPU;
+                                       # "spmd": one process per GPU (spmd.py)
     rs_capacity: int = 8
     l1_enabled: bool = True
     l2_enabled: bool = True
@@ -823,7 +824,7 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         # diagonal solves are latency-bound and leave SMs idle unless more tasks overlap
         import dataclasses
         options = dataclasses.replace(options, n_streams=8 if plan.call.kind == "trsm" else 4)
-    if options.execution not in ("deterministic", "concurrent"):
+    if options.execution not in ("deterministic", "concurrent", "spmd"):
         raise ConfigError(f"unknown execution mode {options.execution!r}")
     if not 1 <= options.n_streams <= 8:
         raise ConfigError("n_streams must be in 1..8")
@@ -831,6 +832,10 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         raise ConfigError("chunk_steps must be >= 1")
     if options.tasks_per_stream < 1:
         raise ConfigError("tasks_per_stream must be >= 1")
+    if options.execution == "spmd":
+        # one process per GPU: every rank of the session runs this same call (spmd.py)
+        from . import spmd
+        return spmd.run_plan_spmd(plan, options, engine, _t_plan=_t_plan)
     topology = topology or discover_topology()
     devs = topology.accelerators()
     if engine is None:

@@ -87,30 +87,39 @@ class FakeEngine:
         self.ev_done[ev] = False
         return ev
 
-    def _enqueue(self, slot, lane, fn, waits):
+    def _enqueue(self, slot, lane, fn, waits, cond=None):
+        """``cond``: extra readiness predicate (a flag another process raises)."""
         ev = self._new_ev()
         for w in waits:
             assert w in self.ev_done, f"wait on unknown event {w}"
-        self.queues.setdefault((slot, lane), []).append((list(waits), fn, ev))
+        self.queues.setdefault((slot, lane), []).append((list(waits), fn, ev, cond))
         return ev
 
     def _step(self) -> bool:
         """Execute the head op of one random runnable stream."""
         ready = [k for k, q in self.queues.items()
-                 if q and all(self.ev_done[w] for w in q[0][0])]
+                 if q and all(self.ev_done[w] for w in q[0][0]) and (q[0][3] is None or q[0][3]())]
         if not ready:
             return False
         k = self.rng.choice(sorted(ready))
-        waits, fn, ev = self.queues[k].pop(0)
+        waits, fn, ev, _ = self.queues[k].pop(0)
         fn()
         self.ev_done[ev] = True
         return True
 
-    def _run_until(self, pred, limit=10_000_000):
+    def _remote_blocked(self) -> bool:
+        return any(q and q[0][3] is not None for q in self.queues.values())
+
+    def _run_until(self, pred, limit=10_000_000, timeout=120.0):
+        import time as _t
+        t0 = _t.perf_counter()
         for _ in range(limit):
             if pred():
                 return
             if not self._step():
+                if self._remote_blocked() and _t.perf_counter() - t0 < timeout:
+                    _t.sleep(1e-4)          # another process will raise the flag
+                    continue
                 assert pred(), "fake GPU deadlock: pending ops wait on events that never fire"
                 return
 
@@ -218,7 +227,10 @@ class FakeEngine:
         return self.ev_done[ev]
 
     def wait_any(self, evs, spin_us=-1):
-        self._run_until(lambda: any(self.ev_done[e] for e in evs))
+        if spin_us is not None and spin_us >= 0 and self._remote_blocked():
+            self._step()
+        else:
+            self._run_until(lambda: any(self.ev_done[e] for e in evs))
         for i, e in enumerate(evs):
             if self.ev_done[e]:
                 return i

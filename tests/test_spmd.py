@@ -1,0 +1,88 @@
+"""One process per GPU (paper_1510_05041_b200/spmd.py): the shared task queue, stations
+with cross-process stealing, first-holder directory with IPC peer copies gated by arrival
+flags, cross-rank TRSM dependencies, and error propagation.
+
+CPU: every rank is a spawned process on the fake engine with /dev/shm arenas (each rank
+checks nothing itself; rank 0 compares the shared output with the oracle).  GPU: the same
+cases with the real engine, several ranks sharing GPU 0 (IPC + stream memory operations on
+hardware)."""
+
+import pytest
+
+import spmd_cases as SC
+from paper_1510_05041_b200 import spmd
+
+CASES = [
+    ("gemm", 192, 160, 64, {}),
+    ("gemm", 200, 130, 64, dict(trans_a=True, trans_b=True, alpha=0.5, beta=-1.0)),
+    ("syrk", 192, 96, 64, {}),
+    ("syr2k", 160, 96, 64, dict(uplo="upper")),
+    ("symm", 160, 160, 64, dict(side="right")),
+    ("trmm", 192, 192, 64, {}),
+    ("trsm", 192, 192, 64, {}),
+    ("trsm", 160, 160, 64, dict(side="right", uplo="upper", trans_a=True)),
+]
+
+
+def _check(outs, world):
+    errs = [o.get("error") for o in outs]
+    assert errs == [None] * world, errs
+    o0 = outs[0]
+    assert o0["max_err"] <= 1e-11 * max(1.0, o0["scale"]), o0
+    for o in outs:
+        # every rank returns the same gathered metrics
+        assert o["tasks"] == o0["tasks"] and o["h2d"] == o0["h2d"]
+        assert sum(o["tasks"].values()) == o["n_tasks"]      # every task exactly once
+        assert o["d2d"] == o["d2d_out"]                     # peer bytes in == out
+
+
+@pytest.mark.parametrize("kind,n,k,tile,extra", CASES)
+def test_spmd_routines_fake_two_ranks(kind, n, k, tile, extra):
+    outs = spmd.launch(2, SC.run_case, kind, n, k, tile, 1, True, None, extra, timeout=600)
+    _check(outs, 2)
+
+
+def test_spmd_gemm_three_ranks_host_bytes_once():
+    outs = spmd.launch(3, SC.run_case, "gemm", 256, 256, 64, 2, True, timeout=600)
+    _check(outs, 3)
+    o = outs[0]
+    # first-holder policy: each input tile crosses the host link once (A + B + C move-in)
+    assert o["h2d"] == (256 * 256 * 3) * 8
+    assert o["host"] == 2 * 16
+    assert o["second_tasks"] == o["n_tasks"]
+
+
+def test_spmd_trsm_three_ranks_small_station():
+    outs = spmd.launch(3, SC.run_case, "trsm", 256, 256, 64, 4, True, dict(rs_capacity=2),
+                       timeout=600)
+    _check(outs, 3)
+
+
+def test_spmd_singular_aborts_every_rank():
+    outs = spmd.launch(2, SC.run_singular, 160, 64, True, timeout=600)
+    assert outs == ["SingularMatrixError", "SingularMatrixError"]
+
+
+def test_spmd_needs_shared_operands():
+    outs = spmd.launch(1, SC.check_shared_required, True, timeout=300)
+    assert outs == ["InvalidArgumentError"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,k,tile,extra", [
+    ("gemm", 1536, 1280, 512, {}),
+    ("syr2k", 1280, 768, 512, {}),
+    ("trmm", 1536, 1536, 512, {}),
+    ("trsm", 1536, 1536, 512, {}),
+])
+def test_spmd_gpu_ranks_share_one_b200(kind, n, k, tile, extra):
+    outs = spmd.launch(2, SC.run_case, kind, n, k, tile, 5, False, None, extra, timeout=900,
+                       devices=[0, 0])
+    _check(outs, 2)
+
+
+@pytest.mark.gpu
+def test_spmd_gpu_three_ranks_trsm():
+    outs = spmd.launch(3, SC.run_case, "trsm", 2048, 2048, 512, 6, False, timeout=900,
+                       devices=[0, 0, 0])
+    _check(outs, 3)
