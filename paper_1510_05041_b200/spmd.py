@@ -812,8 +812,36 @@ def launch(world: int, fn, *args, job: Optional[str] = None, timeout: float = 18
     out = [None] * world
     errs = []
     try:
-        for _ in range(world):
-            rank, status, val = q.get(timeout=timeout)
+        import queue as _queue
+        deadline = time.monotonic() + timeout
+        pending = set(range(world))
+        while pending:
+            try:
+                rank, status, val = q.get(timeout=1.0)
+            except _queue.Empty:
+                # a rank that died without reporting (import error, signal) would otherwise
+                # leave the parent waiting for the full timeout
+                dead = [r for r in pending if procs[r].exitcode is not None]
+                if dead:
+                    time.sleep(0.5)
+                    while True:
+                        try:
+                            rank, status, val = q.get_nowait()
+                        except _queue.Empty:
+                            break
+                        pending.discard(rank)
+                        (errs.append((rank, val)) if status != "ok"
+                         else out.__setitem__(rank, val))
+                    for r in [r for r in pending if procs[r].exitcode is not None]:
+                        errs.append((r, f"exited with code {procs[r].exitcode} without a result"))
+                        pending.discard(r)
+                    if errs:
+                        break
+                if time.monotonic() > deadline:
+                    errs.extend((r, f"no result after {timeout:.0f} s") for r in sorted(pending))
+                    break
+                continue
+            pending.discard(rank)
             if status == "ok":
                 out[rank] = val
             else:
