@@ -13,9 +13,11 @@ Prints ONE JSON line (rank 0).  Legs:
             peak measured live (MEASURED_PEAKS.json has no FP64 figure);
   cpu_baseline  the oracle port of the reference tiled runtime (numpy/OpenBLAS, all host
             cores) on a bounded sample of the same workload.
-Under torchrun (WORLD_SIZE>1) rank 0 drives all N GPUs from one process — BLASX is a
-single-address-space multi-GPU runtime (the L2 tile cache is peer HBM) — and the other
-ranks only join the barriers.
+Under torchrun (WORLD_SIZE>1) every rank drives its own GPU (LOCAL_RANK) through the
+one-process-per-GPU runtime (spmd.py): shared task queue, stations with stealing, and the
+L2 tile cache over peer HBM via CUDA IPC; steps are bracketed by session barriers and the
+step time is the max over ranks.  ``--gpus N`` without torchrun drives N GPUs from one
+process (the single-address-space runtime).
 """
 
 from __future__ import annotations
@@ -189,16 +191,6 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
 
 
-def maybe_init_dist():
-    rank, world = dist_env()
-    if world <= 1:
-        return None
-    import torch.distributed as dist
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    return dist
-
-
 # ----------------------------------------------------------------------------- legs
 
 def run_reference(args, cfg):
@@ -345,69 +337,11 @@ def e2e_leg(args, cfg, eng):
                             for d, v in mt.devices.items()}, call=call)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--chunk", type=int, default=16)
-    ap.add_argument("--streams", type=int, default=0)
-    ap.add_argument("--tasks-per-stream", type=int, default=2)
-    ap.add_argument("--ref-seconds", type=float, default=8.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tile", type=int, default=0, help="override the config's tile size")
-    args = ap.parse_args()
-    cfg = CONFIGS[args.config]
-    if args.tile:
-        cfg = dict(cfg, tile=args.tile, desc=cfg["desc"].replace(f"tile {cfg['tile']}", f"tile {args.tile}"))
-    rank, world = dist_env()
-    dist = maybe_init_dist()
-
-    if args.impl == "reference":
-        if rank == 0:
-            print(json.dumps(run_reference(args, cfg)), flush=True)
-        if dist:
-            dist.barrier()
-        return
-
-    if rank != 0:
-        dist.barrier()   # start
-        dist.barrier()   # end
-        return
-
-    from paper_1510_05041_b200 import _native as NN
-    from paper_1510_05041_b200.engine import get_engine
-    lib = NN.load()
-    NN.require_gpu()
-    f32 = cfg.get("dtype") == "f32"
-    eng = get_engine(list(range(args.gpus)), 4)
-    if os.environ.get("BX_TRSM_LEAF"):
-        NN.check(lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"])), "trsm leaf")
-    peak = C.c_double()
-    NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
-    if dist:
-        dist.barrier()
-
-    with ClockSampler(args.gpus) as clk:
-        if cfg["kind"] == "gemm":
-            val = device_value_leg(args, cfg, eng, lib, NN)
-        else:
-            val = None
-        e2e = e2e_leg(args, cfg, eng)
-    if dist:
-        dist.barrier()
-
-    cpu = None
-    if not args.no_cpu_baseline:
-        cpu = cpu_sample(cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"],
-                         e2e["call"] if cfg["kind"] == "gemm" else make_operands(CONFIGS["cfg2"]),
-                         target_s=10.0)
-
+def result_line(args, cfg, val, e2e, peak_measured, clk, cpu, f32, execution="single process"):
+    """The bench JSON line (shared by the single-process and one-process-per-GPU paths)."""
     flops = e2e["flops"]
     h2d_bw, p2p_bw = 53.0e9, 700e9      # measured (profiles/peaks_r01.json); P2P: nominal-measured
-    peak_tf = peak.value
+    peak_tf = peak_measured
     peak_src = ("measured live: register-only DMMA.8x8x4 loop (bx_fp64_peak_probe); "
                 "MEASURED_PEAKS.json has no FP64 entry")
     if f32:
@@ -450,7 +384,7 @@ def main():
                      "kernel": ("bx::sgemm_tc_kernel (tcgen05.mma kind::tf32, TMEM accumulators, TMA)"
                                 if f32 else "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
                      "peak_source": peak_src,
-                     "fp64_dmma_peak_measured": peak.value,
+                     "fp64_dmma_peak_measured": peak_measured,
                      "flops_per_launch": val["flops_per_launch"] if val else None,
                      "avg_launch_ms": val["avg_launch_ms"] if val else None},
         "gpu_launches": e2e["launches"] + (val["launches"] if val else 0),
@@ -460,7 +394,185 @@ def main():
     }
     if cpu:
         out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    print(json.dumps(out), flush=True)
+    out["execution"] = execution
+    return out
+
+
+# ----------------------------------------------------------------------------- one process per GPU
+
+def spmd_bench(args, cfg):
+    """WORLD_SIZE > 1 (torchrun): every rank drives its own GPU (LOCAL_RANK) through the SPMD
+    runtime (paper_1510_05041_b200/spmd.py: shared task queue, stations with stealing, IPC
+    peer tile cache).  Each step is bracketed by a session barrier and a device sync on
+    every rank; the step time is the max over ranks of the rank's CUDA-event time."""
+    from paper_1510_05041_b200 import RunOptions, run_call, spmd
+    from paper_1510_05041_b200 import _native as NN
+    from paper_1510_05041_b200.engine import get_engine
+    # --ranks-share-gpu: every rank on GPU 0 (exercises the multi-process path on a 1-GPU box)
+    sess = spmd.init(device=0 if args.ranks_share_gpu else None)
+    r, W = sess.rank, sess.world
+    lib = NN.load()
+    NN.require_gpu()
+    f32 = cfg.get("dtype") == "f32"
+    eng = get_engine([r], 4, [sess.device])
+    slot = eng.slot(r)
+    peak = C.c_double()
+    NN.check(lib.bx_fp64_peak_probe(slot, 40000, C.byref(peak)), "peak probe")
+    peak_v = float(sess.allgather(peak.value).min())
+
+    def timed(fn):
+        sess.barrier("step start")
+        eng.device_sync(slot)
+        e0 = eng.record(slot, 0, timing=True)
+        out = fn()
+        e1 = eng.record(slot, 0, timing=True)
+        eng.sync(e1)
+        eng.device_sync(slot)
+        ms = eng.elapsed_ms(e0, e1)
+        eng.release(e0)
+        eng.release(e1)
+        return sess.allreduce_max(ms), ms, out
+
+    clk = ClockSampler(W) if r == 0 else None
+    if clk:
+        clk.__enter__()
+    try:
+        val = None
+        if cfg["kind"] == "gemm":
+            m, n, k = cfg["m"], cfg["n"], cfg["k"]
+            esz = 4 if f32 else 8
+            cols = [n // W + (1 if g < n % W else 0) for g in range(W)]
+            mine = cols[r]
+            ptrs = []
+            for i, nelem in enumerate((m * k, k * mine, m * mine)):
+                p = C.c_uint64()
+                NN.check(lib.bx_dev_alloc(slot, nelem * esz, C.byref(p)), "alloc")
+                fill = lib.bx_dev_fill_uniform_f32 if f32 else lib.bx_dev_fill_uniform
+                NN.check(fill(slot, p.value, nelem, 1234 + 7 * r + i, 0), "fill")
+                ptrs.append(p.value)
+            eng.device_sync(slot)
+            a, b, c = ptrs
+
+            def launch():
+                if f32:
+                    NN.check(lib.bx_sgemm_device(slot, 0, 0, 0, m, mine, k, 1.0, a, m, b, k, 0.0, c, m), "sgemm")
+                else:
+                    NN.check(lib.bx_dgemm_device(slot, 0, 0, 0, m, mine, k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
+            for _ in range(args.warmup):
+                launch()
+            n0 = eng.launches()
+            steps, mine_ms = [], []
+            for _ in range(args.steps):
+                t, own, _ = timed(launch)
+                steps.append(t)
+                mine_ms.append(own)
+            launches = int(sess.allgather(eng.launches() - n0).sum())
+            for p in ptrs:
+                lib.bx_dev_free(slot, p)
+            ms_step = statistics.mean(steps)
+            own_ms = statistics.mean(mine_ms)
+            flops_mine = 2.0 * m * mine * k
+            # dominant-kernel roofline: rank-average launch time and flops
+            avg_ms = float(sess.allgather(own_ms).mean())
+            avg_fl = float(sess.allgather(flops_mine).mean())
+            val = dict(value=2.0 * m * n * k / (ms_step / 1e3) / 1e12, ms_per_step=ms_step,
+                       launches=launches, kernel_tflops=avg_fl / (avg_ms / 1e3) / 1e12,
+                       avg_launch_ms=avg_ms, flops_per_launch=avg_fl)
+
+        call = make_operands(cfg, seed=0) if r == 0 else None
+        call = sess.share_call(call)
+        for mt in (call.a, call.b, call.c):
+            if mt is not None:
+                eng.register_host(mt.matrix.storage)   # page-locking excluded from timing
+        opts = RunOptions(execution="spmd", chunk_steps=args.chunk, n_streams=args.streams,
+                          tasks_per_stream=args.tasks_per_stream)
+        res = None
+        for _ in range(args.warmup):
+            res = run_call(call, options=opts)
+        n0 = eng.launches()
+        times = []
+        for _ in range(args.steps):
+            t, _, res = timed(lambda: run_call(call, options=opts))
+            times.append(t)
+        launches = int(sess.allgather(eng.launches() - n0).sum())
+    finally:
+        if clk:
+            clk.__exit__(None, None, None)
+    ms = statistics.mean(times)
+    mt = res.metrics
+    e2e = dict(value=res.plan.total_flops / (ms / 1e3) / 1e12, ms=ms, flops=res.plan.total_flops,
+               launches=launches, sweep=[], h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(),
+               p2p=mt.total_d2d_bytes(), l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
+               per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
+                           for d, v in mt.devices.items()})
+    sess.barrier("bench end")
+    if r == 0:
+        line = result_line(args, cfg, val, e2e, peak_v, clk, None, f32,
+                           execution=f"one process per GPU ({W} ranks, spmd runtime)")
+        print(json.dumps(line), flush=True)
+    sess.barrier("bench printed")
+    spmd.shutdown()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--chunk", type=int, default=16)
+    ap.add_argument("--streams", type=int, default=0)
+    ap.add_argument("--tasks-per-stream", type=int, default=2)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ranks-share-gpu", action="store_true",
+                    help="torchrun test mode: all ranks use GPU 0 (numbers are not scaling)")
+    ap.add_argument("--tile", type=int, default=0, help="override the config's tile size")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.tile:
+        cfg = dict(cfg, tile=args.tile, desc=cfg["desc"].replace(f"tile {cfg['tile']}", f"tile {args.tile}"))
+    rank, world = dist_env()
+    if args.gpus != world and world > 1:
+        log(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
+        args.gpus = world
+
+    if args.impl == "reference":
+        # the reference's CPU path: rank 0 alone runs it, the other ranks exit without work
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+
+    if world > 1:
+        spmd_bench(args, cfg)
+        return
+
+    from paper_1510_05041_b200 import _native as NN
+    from paper_1510_05041_b200.engine import get_engine
+    lib = NN.load()
+    NN.require_gpu()
+    f32 = cfg.get("dtype") == "f32"
+    eng = get_engine(list(range(args.gpus)), 4)
+    if os.environ.get("BX_TRSM_LEAF"):
+        NN.check(lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"])), "trsm leaf")
+    peak = C.c_double()
+    NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
+
+    with ClockSampler(args.gpus) as clk:
+        if cfg["kind"] == "gemm":
+            val = device_value_leg(args, cfg, eng, lib, NN)
+        else:
+            val = None
+        e2e = e2e_leg(args, cfg, eng)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"],
+                         e2e["call"] if cfg["kind"] == "gemm" else make_operands(CONFIGS["cfg2"]),
+                         target_s=10.0)
+
+    print(json.dumps(result_line(args, cfg, val, e2e, peak.value, clk, cpu, f32)), flush=True)
 
 
 if __name__ == "__main__":

@@ -200,6 +200,14 @@ class Session:
         self.barrier("allreduce done")
         return out
 
+    def allgather(self, value: float) -> np.ndarray:
+        """Every rank's ``value`` (collective), as a float64 array indexed by rank."""
+        self.red[self.rank] = value
+        self.barrier("allgather")
+        out = self.red.copy()
+        self.barrier("allgather done")
+        return out
+
     def next_call(self) -> int:
         """All ranks advance the call sequence together (called between barriers)."""
         return int(self.hdr[2]) + 1
