@@ -32,7 +32,12 @@ import sys
 import threading
 import time
 
-import numpy as np
+# torchrun exports OMP_NUM_THREADS=1 to every rank; the CPU baseline / reference arm should
+# use all host cores (OpenBLAS reads OPENBLAS_NUM_THREADS before OMP_NUM_THREADS at import)
+if "OPENBLAS_NUM_THREADS" not in os.environ:
+    os.environ["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -169,6 +174,11 @@ def cpu_sample(cfg, call, target_s=12.0):
     rng = np.random.default_rng(1)
     nt = -(-cfg["m"] // t)
     flops_per_tile = 2 * t * t * cfg["k"]
+    try:   # all host threads, whatever the launcher exported
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count(), user_api="blas")
+    except Exception:
+        pass
     # warm-up one tile (OpenBLAS init), then as many tiles as fit target_s
     tiled.run_tiles_subset("gemm", a, c, b, tile_size=t, tiles=[(0, 0)], alpha=cfg["alpha"],
                            beta=cfg["beta"])
