@@ -17,6 +17,7 @@
  *                              via the triangle epilogue
  *   bx_trsm_tile               kernels.py:105-161 trsm_solve
  *   bx_materialize             kernels.py:164-211 (_masked_triangle / _symmetrized)
+ *   bx_axpy_tile               kernels.py:40-41 _accumulate's beta*C term, applied late
  *   bx_event_*                 devices.py:150-166 sync_streams / drain_time; trace times
  *   bx_last_error              errors.py exception messages
  *
@@ -97,6 +98,11 @@ int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int 
 int bx_materialize(int dev, int stream, int mode_sym, int upper, int trans, int unit, int n,
                    uint64_t a_off, int lda, uint64_t dst_off, int ldd, int n_wait, const int* wait,
                    int* ev_out);
+/* dst (h x w) += beta * src (fp64 or fp32 by elem_bytes): the deferred beta*C term of a
+ * task whose first GEMM launch ran with beta = 0, so the C tile's host copy is needed only
+ * by this last kernel (kernels.py:49-58 applies beta once; same value, C0 read late) */
+int bx_axpy_tile(int dev, int stream, int elem_bytes, int h, int w, double beta, uint64_t src_off,
+                 int src_ld, uint64_t dst_off, int dst_ld, int n_wait, const int* wait, int* ev_out);
 /* singular flag set by bx_trsm_tile kernels of this device since the last reset */
 int bx_singular_flag(int dev, int reset, int* flag);
 

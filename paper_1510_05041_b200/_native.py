@@ -53,6 +53,7 @@ _SIGS = {
     "bx_sgemm_device": [_i, _i, _i, _i, _i, _i, _i, C.c_float, _u64, _i, _u64, _i, C.c_float, _u64, _i],
     "bx_trsm_tile": [_i, _i, _i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_materialize": [_i, _i, _i, _i, _i, _i, _i, _u64, _i, _u64, _i, _i, _pi, _pi],
+    "bx_axpy_tile": [_i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_singular_flag": [_i, _i, _pi],
     "bx_event_record": [_i, _i, _i, _pi],
     "bx_event_query": [_i],

@@ -789,6 +789,34 @@ int bx_materialize(int dev, int stream, int mode_sym, int upper, int trans, int 
   return finish(dev, s, ev_out);
 }
 
+// dst (h x w) += beta * src: the deferred beta*C0 term of a task whose first GEMM launch
+// ran with beta = 0 (the C0 tile's host copy is then off the task's critical path).
+// One warp per 32 rows x 8 columns; both tiles column-major in the arena.
+int bx_axpy_tile(int dev, int stream, int elem_bytes, int h, int w, double beta, uint64_t src_off, int src_ld,
+                 uint64_t dst_off, int dst_ld, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  if (h < 0 || w < 0 || src_ld < h || dst_ld < h || (elem_bytes != 8 && elem_bytes != 4))
+    return set_err(BX_EINVAL, "axpy: bad extents");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  if (h > 0 && w > 0) {
+    dim3 blk(32, 8), grd((h + 31) / 32, (w + 7) / 8);
+    if (elem_bytes == 8)
+      bx::axpy_tile_kernel<double><<<grd, blk, 0, s>>>((double*)(D->arena + dst_off), dst_ld,
+                                                   (const double*)(D->arena + src_off), src_ld, h, w, beta);
+    else
+      bx::axpy_tile_kernel<float><<<grd, blk, 0, s>>>((float*)(D->arena + dst_off), dst_ld,
+                                                  (const float*)(D->arena + src_off), src_ld, h, w, (float)beta);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return finish(dev, s, ev_out);
+}
+
 int bx_singular_flag(int dev, int reset, int* flag) {
   Device* D = dev_of(dev);
   if (!D) return set_err(BX_EINVAL, "bad device");

@@ -145,6 +145,14 @@ __global__ void materialize_kernel(const double* __restrict__ a, int lda, double
   dst[(size_t)c * ldd + r] = v;
 }
 
+template <typename T>
+__global__ void axpy_tile_kernel(T* __restrict__ dst, int ldd, const T* __restrict__ src, int lds, int h, int w,
+                                 T beta) {
+  const int r = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.y * 8 + threadIdx.y;
+  if (r < h && c < w) dst[(size_t)c * ldd + r] += beta * src[(size_t)c * lds + r];
+}
+
 __global__ void scale_kernel(double* __restrict__ b, int ld, int h, int w, double alpha) {
   int r = blockIdx.x * 32 + threadIdx.x;
   int c = blockIdx.y * 8 + threadIdx.y;

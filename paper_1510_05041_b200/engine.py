@@ -201,6 +201,14 @@ class CudaEngine:
                 "materialize")
         return ev.value
 
+    def axpy(self, slot, stream, esz, h, w, beta, src_off, src_ld, dst_off, dst_ld,
+             waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_axpy_tile(slot, stream, esz, h, w, float(beta), src_off, src_ld,
+                                      dst_off, dst_ld, nw, wp, C.byref(ev)), "axpy tile")
+        return ev.value
+
     def singular(self, slot, reset=True) -> bool:
         f = C.c_int(0)
         N.check(self.lib.bx_singular_flag(slot, int(reset), C.byref(f)))

@@ -43,19 +43,31 @@ class TrsmOp(NamedTuple):
     flops: int
 
 
+class AxpyOp(NamedTuple):
+    beta: float          # C += beta * C0 (C0 = the output tile's host values, fetched late)
+
+
 class Program(NamedTuple):
     ops: tuple
     scratch_n: tuple     # order of each scratch tile
+    defer_c: bool = False  # C move-in deferred to a final AxpyOp (first GEMM runs beta=0)
 
 
 def scratch_key(i: int) -> tuple:
     return ("#scratch", i)
 
 
-def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0) -> Program:
+def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
+                 defer_c: bool = False) -> Program:
     """``first_chunk`` (if > 0) caps the task's first GEMM launch so its kernel can start
-    as soon as the first few input tiles have landed (pipeline ramp-up)."""
-    ckey = (chunk_steps, first_chunk)
+    as soon as the first few input tiles have landed (pipeline ramp-up).
+
+    ``defer_c``: for a task whose C tile must be moved in only for the beta*C term (plain
+    GEMM updates, no triangle epilogue, no solve), the first GEMM launch runs with beta = 0
+    (C is not read, kernels.py:40-41) and a final AxpyOp adds beta*C0 from a separately
+    fetched copy — beta is still applied exactly once (routines.py:211-215), but the
+    task's kernels no longer wait for the C tile's host copy."""
+    ckey = (chunk_steps, first_chunk, defer_c)
     cache = getattr(task, "_bx_prog", None)
     if cache is not None and cache[0] == ckey:
         return cache[1]
@@ -115,6 +127,15 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0) -> Pr
         else:
             raise ValueError(f"unknown step kind {kind!r}")
     flush()
-    prog = Program(tuple(ops), tuple(scratch))
+    deferred = False
+    if defer_c and task.needs_c_move_in:
+        gemms = [i for i, o in enumerate(ops) if type(o) is GemmOp]
+        if (gemms and all(type(o) is not TrsmOp for o in ops)
+                and all(ops[i].tri == 0 for i in gemms) and ops[gemms[0]].beta != 0.0):
+            g = ops[gemms[0]]
+            ops[gemms[0]] = g._replace(beta=0.0)
+            ops.append(AxpyOp(g.beta))
+            deferred = True
+    prog = Program(tuple(ops), tuple(scratch), deferred)
     task._bx_prog = (ckey, prog)
     return prog

@@ -43,7 +43,7 @@ from .errors import (ArenaOutOfMemoryError, CapacityDeadlockError, ConfigError,
 from .memory import Arena
 from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
                        TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
-from .program import GemmOp, MatOp, compile_task, scratch_key
+from .program import AxpyOp, GemmOp, MatOp, compile_task, scratch_key
 from .tiling import device_ld
 
 WORKING_SET_TILES = 12   # reference floor (scheduler.py:49-52): 4 tasks x (C + 2 inputs)
@@ -80,7 +80,13 @@ class RunOptions:
     n_streams: int = 0                 # compute streams per GPU; 0 = auto (4, TRSM 8)
     chunk_steps: int = 16              # k-steps fused per kernel launch
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
-    first_chunk_steps: int = 4         # shorter first launch per task (ramp-up); 0 = off
+    first_chunk_steps: int = 0         # shorter first launch per task; 0 = off
+    ramp_tasks: int = -1               # start-up batch: the first N tasks a GPU starts run
+    ramp_chunk_steps: int = 4          # in extra slots with ramp_chunk_steps-long launches,
+                                       # advancing k-major together while their panels
+                                       # stream in (-1 = auto, 0 = off; resident mode only)
+    defer_c_move_in: bool = True       # beta*C0 added by a final axpy launch, so a task's
+                                       # GEMMs do not wait for its C tile (program.py)
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
@@ -204,7 +210,7 @@ class _Active:
     """A task in flight on one compute stream."""
     __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
                  "events", "last_ev", "done_ev", "pending_waits", "flops", "prog", "res",
-                 "next_op", "lazy", "misses", "misses_epoch")
+                 "next_op", "lazy", "misses", "misses_epoch", "c_pending", "c0_off", "ramp")
 
     def __init__(self, entry, stream):
         self.entry = entry
@@ -219,6 +225,9 @@ class _Active:
         self.done_ev = None      # write-back completion
         self.pending_waits = []  # waits to attach to the next launch (C move-in)
         self.flops = 0
+        self.c_pending = False   # C move-in not yet enqueued
+        self.c0_off = -1         # deferred C move-in buffer (program.defer_c)
+        self.ramp = False        # part of the start-up batch (extra slot, short launches)
 
 
 class _GpuWorker:
@@ -241,7 +250,8 @@ class _GpuWorker:
         # active slots: tasks_per_stream tasks may be queued on each compute stream, so the
         # next task's copies and kernels are already enqueued when the current one drains
         self.n_streams = opts.n_streams
-        self.active = [None] * (opts.n_streams * opts.tasks_per_stream)
+        self.base_slots = opts.n_streams * opts.tasks_per_stream
+        self.active = [None] * (self.base_slots + max(0, opts.ramp_tasks))
         self.l1_hits = self.l2_hits = self.host_fetches = 0
         self.tasks_done = 0
         self._cur: Optional[_Active] = None
@@ -258,6 +268,7 @@ class _GpuWorker:
         self._sync_epoch = 0
         self._task_misses = 0
         self.chunk_steps = opts.chunk_steps
+        self._ramp_left = max(0, opts.ramp_tasks)
         grp = runtime.topology.peer_group_of(desc)
         self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
                                       if d.device_id != desc.device_id
@@ -394,13 +405,19 @@ class _GpuWorker:
 
     def fill(self) -> bool:
         fresh = []
+        # ramp tasks (start-up batch) use extra slots; the others are capped at base_slots
+        normal = sum(1 for a in self.active if a is not None and not a.ramp)
         for s, act in enumerate(self.active):
             if act is not None:
                 continue
+            if self._ramp_left <= 0 and normal >= self.base_slots:
+                break
             entry = self._next_entry()
             if entry is None:
                 break
-            fresh.append(self._begin(entry, s))
+            act = self._begin(entry, s)
+            normal += not act.ramp
+            fresh.append(act)
         # one launch group per fresh task per round (k-major fetch order across them)
         pending = fresh
         while pending:
@@ -599,15 +616,21 @@ class _GpuWorker:
             h, w = out.phys_height, out.phys_width
             act.c_ld = device_ld(h)
             act.c_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
-            if task.needs_c_move_in:
-                desc, r0, c0 = self._host_of(out)
-                ev = self._timed(LANE_H2D, lambda wt: self.eng.h2d(
-                    self.slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
-                    h * w * self.esz)
-                act.events.append(ev)
-                act.pending_waits.append(ev)
-                self.dm.h2d_bytes += h * w * self.esz
-            act.prog = compile_task(task, self.plan.call, self.chunk_steps, opts.first_chunk_steps)
+            # the C move-in is enqueued with the task's first launch group (_advance), so
+            # the H2D queue interleaves a fresh batch's C tiles with its first panels
+            act.c_pending = task.needs_c_move_in
+            chunk = self.chunk_steps
+            if self._ramp_left > 0:
+                self._ramp_left -= 1
+                act.ramp = True
+                chunk = min(opts.ramp_chunk_steps, chunk)
+            act.prog = compile_task(task, self.plan.call, chunk, opts.first_chunk_steps,
+                                    opts.defer_c_move_in)
+            if act.prog.defer_c:
+                # C0 gets its own buffer, fetched with the task's last launch group
+                act.c_pending = False
+                act.c0_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
+                act.scratch.append(act.c0_off)
             act.lazy = opts.l1_enabled and not self.resident
             act.misses = 0
             act.misses_epoch = self._sync_epoch
@@ -643,12 +666,23 @@ class _GpuWorker:
         self._cur = act
         self._task_misses = act.misses
         try:
+            if act.c_pending:
+                act.c_pending = False
+                desc, r0, c0 = self._host_of(out)
+                ev = self._timed(LANE_H2D, lambda wt: eng.h2d(
+                    slot, act.c_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
+                    h * w * self.esz)
+                act.events.append(ev)
+                act.pending_waits.append(ev)
+                self.dm.h2d_bytes += h * w * self.esz
             res = act.res
             i = act.next_op
             while i < len(ops):
                 op = ops[i]
                 i += 1
-                if act.lazy:
+                if type(op) is AxpyOp:
+                    pass
+                elif act.lazy:
                     if act.misses_epoch != self._sync_epoch:
                         # a pressure sync released this task's earlier pins: forget them
                         for k in [k for k in res if k[0] != "#scratch"]:
@@ -682,6 +716,18 @@ class _GpuWorker:
                         False if op.sym else call.trans_a, (not op.sym) and call.diag == "unit",
                         op.n, ao, al, so, sl, wt), [aw] if aw is not None else [], "KERNEL", 0, -1)
                     act.events.append(ev)
+                elif type(op) is AxpyOp:
+                    desc, r0, c0 = self._host_of(out)
+                    c0_ev = self._timed(LANE_H2D, lambda wt: eng.h2d(
+                        slot, act.c0_off, act.c_ld, desc, r0, c0, h, w, wt), (), "H2D",
+                        h * w * self.esz)
+                    act.events.append(c0_ev)
+                    self.dm.h2d_bytes += h * w * self.esz
+                    ev = self._timed(stream, lambda wt, op=op: eng.axpy(
+                        slot, stream, self.esz, h, w, op.beta, act.c0_off, act.c_ld, act.c_off,
+                        act.c_ld, wt), [c0_ev], "KERNEL", 0, -1)
+                    self._launched(act, ev)
+                    break
                 else:   # TrsmOp
                     ao, al, aw = res[op.key]
                     waits = ([aw] if aw is not None else []) + act.pending_waits
@@ -806,11 +852,23 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
         per_col_tile = rows_full * device_ld(t) + (device_ld(rem) if rem else 0)
         want += -(-per_col_tile * t * col_tiles * esz // 256) * 256 + 256 * col_tiles * (rows_full + 1)
     per_tile = device_ld(t) * t * esz
-    want += (options.n_streams * options.tasks_per_stream + 2) * 2 * per_tile + (64 << 20)
+    slots = options.n_streams * options.tasks_per_stream + max(0, options.ramp_tasks)
+    want += (slots + 2) * 2 * per_tile + (64 << 20)
     if free_bytes is None:
         return want
     cap = int(free_bytes * 0.9) - (1 << 30)
     return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
+
+
+def resolve_ramp(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOptions:
+    """ramp_tasks=-1 (auto): a start-up batch of up to 32 tasks per GPU, but at most a
+    quarter of each GPU's share of the plan so the dynamic schedule (stations, stealing,
+    L2 locality) keeps its freedom at high GPU counts."""
+    if options.ramp_tasks >= 0:
+        return options
+    import dataclasses
+    ramp = min(32, len(plan.tasks) // (4 * max(1, n_devices)))
+    return dataclasses.replace(options, ramp_tasks=ramp if ramp >= 4 else 0)
 
 
 def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
@@ -838,6 +896,7 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         return spmd.run_plan_spmd(plan, options, engine, _t_plan=_t_plan)
     topology = topology or discover_topology()
     devs = topology.accelerators()
+    options = resolve_ramp(plan, options, len(devs))
     if engine is None:
         engine = get_engine([d.device_id for d in devs], options.n_streams,
                             [d.device_id if d.cuda_ordinal is None else d.cuda_ordinal for d in devs])
@@ -884,6 +943,7 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     for w in workers:
         w.resident = resident[w.slot] and options.l1_enabled
         if not w.resident:
+            w._ramp_left = 0      # the start-up batch is for resident arenas only
             # an evicting arena must hold every in-flight task's C and one launch's inputs
             tiles = caps[w.slot] // per_tile
             inflight = options.n_streams * options.tasks_per_stream

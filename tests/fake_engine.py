@@ -195,6 +195,14 @@ class FakeEngine:
                 self.flag[slot] = True
         return self._enqueue(slot, stream, fn, waits)
 
+    def axpy(self, slot, stream, esz, h, w, beta, src_off, src_ld, dst_off, dst_ld, waits=()):
+        self.n_launches += 1
+        view = self._view32 if esz == 4 else self._view
+
+        def fn():
+            view(slot, dst_off, dst_ld, h, w)[:, :] += beta * view(slot, src_off, src_ld, h, w)
+        return self._enqueue(slot, stream, fn, waits)
+
     def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
                     waits=()):
         self.n_launches += 1

@@ -190,3 +190,27 @@ def test_resident_mode_multi_device(kind):
     assert m.total_d2d_bytes() == sum(d.d2d_out_bytes for d in m.devices.values())
     if kind == "gemm":
         assert m.l2_hits > 0
+
+
+@pytest.mark.parametrize("defer", [False, True])
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] in ("gemm", "syrk", "syr2k", "symm")],
+                         ids=lambda c: c["name"])
+def test_deferred_c_move_in_matches_reference(case, defer):
+    """beta*C0 applied by a final axpy launch (first GEMM at beta=0) vs the C tile moved in
+    before the first launch: both match the reference output; diagonal rank-k tasks
+    (triangle epilogue) keep the move-in, so the unstored triangle is written back intact."""
+    from paper_1510_05041_b200.program import AxpyOp, compile_task
+    call = call_of(case)
+    eng = FakeEngine(2, seed=5)
+    res = run_call(call, topo(2), RunOptions(chunk_steps=2, defer_c_move_in=defer,
+                                             ramp_tasks=3, ramp_chunk_steps=1), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-12, atol=1e-12)
+    for t in res.plan.tasks:
+        prog = compile_task(t, res.plan.call, 2, 0, defer)
+        has_axpy = any(type(o) is AxpyOp for o in prog.ops)
+        if not defer or not t.needs_c_move_in:
+            assert not has_axpy
+        elif any(getattr(o, "tri", 0) for o in prog.ops):
+            assert not has_axpy               # triangle epilogue: C moved in first
+        else:
+            assert has_axpy and prog.ops[-1] == AxpyOp(res.plan.call.beta)

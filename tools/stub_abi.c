@@ -31,6 +31,8 @@ int bx_trsm_tile(int d, int s, int r, int u, int t, int un, int h, int w, double
                  uint64_t b, int lb, int n, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_materialize(int d, int s, int m, int u, int t, int un, int n, uint64_t a, int la, uint64_t o, int lo,
                    int nw, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_axpy_tile(int d, int s, int e, int h, int w, double be, uint64_t a, int la, uint64_t o, int lo,
+                 int nw, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_singular_flag(int d, int r, int *f) { *f = 0; return 0; }
 int bx_event_record(int d, int s, int t, int *ev) { return EV(ev); }
 int bx_event_query(int ev) { return 0; }
