@@ -128,9 +128,11 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
                     uint64_t a, int lda, uint64_t b, int ldb, double beta, uint64_t c, int ldc);
 /* tuning knob: tile configuration of the FP64 task GEMM (0 default; 1, 2 alternates) */
 int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 deep, 3 slack-2 */
-/* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 128); larger
+/* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 256); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);
+/* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16 or 32; default 16) */
+int bx_set_trsm_rhs(int nr);
 /* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile */
 int bx_set_sgemm_variant(int variant);
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha,

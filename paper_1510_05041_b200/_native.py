@@ -74,6 +74,7 @@ _SIGS = {
     "bx_fp64_peak_probe": [_i, _i, C.POINTER(C.c_double)],
     "bx_set_gemm_variant": [_i],
     "bx_set_trsm_leaf": [_i],
+    "bx_set_trsm_rhs": [_i],
     "bx_set_sgemm_variant": [_i],
     "bx_last_error": [C.c_char_p, _i],
     "bx_ipc_arena_handle": [_i, _p, _pu64],

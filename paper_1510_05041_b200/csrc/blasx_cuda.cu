@@ -156,7 +156,8 @@ bool need_attr(const void* kernel) {
 }
 
 int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
-int g_trsm_leaf = 128;   // triangle order solved by a leaf kernel; larger ones recurse
+int g_trsm_rhs = 16;     // right-hand sides per CTA of the TRSM panel kernel (8/16/32)
+int g_trsm_leaf = 256;   // triangle order solved by a leaf kernel; larger ones recurse
 
 template <class Cfg, bool TA, bool TB>
 int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s) {
@@ -367,6 +368,22 @@ int scale_raw(cudaStream_t s, double* b, int ld, int h, int w, double alpha) {
   return BX_OK;
 }
 
+template <int NR>
+int launch_panel(cudaStream_t s, const bx::TrsmArgs& t) {
+  constexpr int YP = bx::PanelCfg<NR>::YP;
+  size_t smem = (size_t)t.n * YP * sizeof(double);
+  if (smem > 200 * 1024) return set_err(BX_EINVAL, "trsm panel: triangle too large for this RHS width");
+  if (need_attr((const void*)bx::trsm_panel_kernel<NR>)) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::trsm_panel_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+  }
+  int grid = (t.nrhs + NR - 1) / NR;
+  bx::trsm_panel_kernel<NR><<<grid, bx::T_THREADS, smem, s>>>(t);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return BX_OK;
+}
+
 int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int h, int w, double alpha,
               const double* a, int lda, double* b, int ldb, int* flag) {
   bx::TrsmArgs t{};
@@ -384,13 +401,11 @@ int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int
     CUDA_TRY(cudaGetLastError());
     return BX_OK;
   }
-  size_t smem = (size_t)t.n * bx::T_YP * sizeof(double);
-  if (need_attr((const void*)bx::trsm_panel_kernel)) {
-    CUDA_TRY(cudaFuncSetAttribute(bx::trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  bx::T_NMAX * bx::T_YP * (int)sizeof(double)));
+  switch (g_trsm_rhs) {
+    case 8: { int rc = launch_panel<8>(s, t); if (rc) return rc; break; }
+    case 32: { int rc = launch_panel<32>(s, t); if (rc) return rc; break; }
+    default: { int rc = launch_panel<16>(s, t); if (rc) return rc; break; }
   }
-  int grid = (t.nrhs + bx::T_NRHS - 1) / bx::T_NRHS;
-  bx::trsm_panel_kernel<<<grid, bx::T_THREADS, smem, s>>>(t);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return BX_OK;
@@ -994,6 +1009,12 @@ int bx_set_gemm_variant(int v) {
 int bx_set_sgemm_variant(int v) {
   if (v < 0 || v > 1) return set_err(BX_EINVAL, "sgemm variant must be 0 or 1");
   g_sgemm_variant = v;
+  return BX_OK;
+}
+
+int bx_set_trsm_rhs(int nr) {
+  if (nr != 8 && nr != 16 && nr != 32) return set_err(BX_EINVAL, "trsm panel RHS width must be 8, 16 or 32");
+  g_trsm_rhs = nr;
   return BX_OK;
 }
 

@@ -7,10 +7,10 @@
 //     E = op(A);  left:  E X = alpha B        right: X E = alpha B  <=>  E^T X^T = alpha B^T
 //     swap = trans ^ right      (L(i,j) reads A(j,i) instead of A(i,j))
 //     rev  = left ? eff_upper : !eff_upper     (backward substitution = forward on n-1-i)
-// Each CTA owns 8 right-hand sides (columns of B for left, rows for right) for the whole
-// triangle order n, holds them in shared memory, and walks the diagonal in 32-row
-// blocks: substitution on the 32x32 diagonal block (one warp per RHS, division by the
-// diagonal exactly like the reference; unit diagonal never read), then the trailing
+// Each CTA owns NR (8/16/32) right-hand sides (columns of B for left, rows for right) for
+// the whole triangle order n, holds them in shared memory, and walks the diagonal in
+// 32-row blocks: substitution on the 32x32 diagonal block (warps over RHS, division by
+// the diagonal exactly like the reference; unit diagonal never read), then the trailing
 // rows are updated with DMMA (m8n8k4 f64) against the solved block.  alpha is applied
 // once, on load (kernels.py:124-125).  An exact zero on a non-unit diagonal sets the
 // device-visible singular flag (kernels.py:105-109) -> SingularMatrixError on the host.
@@ -19,7 +19,7 @@
 
 namespace bx {
 
-constexpr int T_NRHS = 8, T_BLK = 32, T_THREADS = 256, T_YP = 12, T_NMAX = 2048;
+constexpr int T_BLK = 32, T_THREADS = 256, T_NMAX = 2048;
 
 struct TrsmArgs {
   const double* a;
@@ -40,84 +40,135 @@ __device__ __forceinline__ double* trsm_Y(const TrsmArgs& t, int i, int col) {
   return t.right ? t.b + (size_t)ii * t.ldb + col : t.b + (size_t)col * t.ldb + ii;
 }
 
+// Y row pitch for NR right-hand sides: NR + 4 doubles (== 4 mod 16) keeps the DMMA
+// B-fragment reads (4 rows x 8 RHS per half-warp) bank-conflict free.
+template <int NR>
+struct PanelCfg {
+  static constexpr int YP = NR + 4;
+  static constexpr int NF = NR / 8;   // 8-wide RHS fragments per DMMA row fragment
+};
+
+// NR right-hand sides per CTA.  More RHS per CTA amortise each global load of L in the
+// trailing update over NR/8 DMMAs and halve the CTAs (SM time) a solve occupies; the
+// substitution phase loops warps over the RHS.
+template <int NR>
 __global__ void __launch_bounds__(T_THREADS) trsm_panel_kernel(const __grid_constant__ TrsmArgs t) {
-  extern __shared__ __align__(16) double ys[];      // [n][T_YP]
+  constexpr int YP = PanelCfg<NR>::YP, NF = PanelCfg<NR>::NF;
+  extern __shared__ __align__(16) double ys[];      // [n][YP]
   __shared__ double ls[T_BLK * (T_BLK + 1)];         // ls[j*(33)+r] = L(i0+r, i0+j)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int col0 = blockIdx.x * T_NRHS;
+  const int col0 = blockIdx.x * NR;
   const int n = t.n;
 
-  for (int idx = tid; idx < n * T_NRHS; idx += T_THREADS) {
-    int c = t.right ? idx % T_NRHS : idx / n;
-    int i = t.right ? idx / T_NRHS : idx % n;
+  for (int idx = tid; idx < n * NR; idx += T_THREADS) {
+    int c = t.right ? idx % NR : idx / n;
+    int i = t.right ? idx / NR : idx % n;
     int col = col0 + c;
-    ys[i * T_YP + c] = (col < t.nrhs) ? t.alpha * *trsm_Y(t, i, col) : 0.0;
+    ys[i * YP + c] = (col < t.nrhs) ? t.alpha * *trsm_Y(t, i, col) : 0.0;
   }
   __syncthreads();
 
   const int g = lane >> 2, q = lane & 3;
+  // diagonal block i0 is loaded into registers one block step ahead (its global loads
+  // overlap the previous step's trailing update) and stored to ls after that step's barrier
+  constexpr int DV = T_BLK * T_BLK / T_THREADS;
+  double v[DV];
+  auto load_diag = [&](int i0) {
+    const int nb = min(T_BLK, n - i0);
+#pragma unroll
+    for (int u = 0; u < DV; ++u) {
+      const int idx = tid + u * T_THREADS, j = idx / T_BLK, r = idx % T_BLK;
+      v[u] = (r < nb && j < nb && r >= j && !(t.unit && r == j)) ? trsm_L(t, i0 + r, i0 + j) : 0.0;
+    }
+  };
+  load_diag(0);
   for (int i0 = 0; i0 < n; i0 += T_BLK) {
     const int nb = min(T_BLK, n - i0);
-    {
-      double v[T_BLK * T_BLK / T_THREADS];
 #pragma unroll
-      for (int q = 0; q < T_BLK * T_BLK / T_THREADS; ++q) {
-        const int idx = tid + q * T_THREADS, j = idx / T_BLK, r = idx % T_BLK;
-        v[q] = (r < nb && j < nb && r >= j && !(t.unit && r == j)) ? trsm_L(t, i0 + r, i0 + j) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < T_BLK * T_BLK / T_THREADS; ++q) {
-        const int idx = tid + q * T_THREADS;
-        ls[(idx / T_BLK) * (T_BLK + 1) + idx % T_BLK] = v[q];
-      }
+    for (int u = 0; u < DV; ++u) {
+      const int idx = tid + u * T_THREADS;
+      ls[(idx / T_BLK) * (T_BLK + 1) + idx % T_BLK] = v[u];
     }
     __syncthreads();
     {
-      // substitution on the diagonal block: warp -> RHS, lane -> row
+      // substitution on the diagonal block: warp -> RHS (NR / 8 each), lane -> row; the
+      // reference divides by the diagonal (kernels.py:140-159), so do we
       const int r = lane;
-      double y = (r < nb) ? ys[(i0 + r) * T_YP + warp] : 0.0;
       double inv = 1.0;
       if (!t.unit && r < nb) {
         const double dd = ls[r * (T_BLK + 1) + r];
         if (dd == 0.0) atomicOr(t.flag, 1);
         inv = 1.0 / dd;
       }
+      double y[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) y[f] = (r < nb) ? ys[(i0 + r) * YP + warp + 8 * f] : 0.0;
       for (int j = 0; j < nb; ++j) {
-        if (r == j && !t.unit) y *= inv;
-        double x = __shfl_sync(0xffffffffu, y, j);
-        if (r > j) y = y - ls[j * (T_BLK + 1) + r] * x;
+        const double l = (r > j) ? ls[j * (T_BLK + 1) + r] : 0.0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          if (r == j && !t.unit) y[f] *= inv;
+          const double x = __shfl_sync(0xffffffffu, y[f], j);
+          y[f] = fma(-l, x, y[f]);
+        }
       }
-      if (r < nb) ys[(i0 + r) * T_YP + warp] = y;
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+        if (r < nb) ys[(i0 + r) * YP + warp + 8 * f] = y[f];
     }
     __syncthreads();
-    // trailing update: Y[r] -= L(r, i0:i0+nb) * Y(i0:i0+nb) for r >= i0+nb (DMMA m8n8k4)
+    if (i0 + T_BLK < n) load_diag(i0 + T_BLK);
+    // trailing update: Y[r] -= L(r, i0:i0+nb) * Y(i0:i0+nb) for r >= i0+nb (DMMA m8n8k4).
+    // A warp takes its row fragments G at a time and issues all their L loads before the
+    // first DMMA (one L2 round trip per G fragments); one L fragment feeds NF DMMAs.
+    constexpr int G = 4;
     const int rbeg = i0 + nb;
     const int nfr = (n - rbeg + 7) / 8;
-    for (int f = warp; f < nfr; f += T_THREADS / 32) {
-      const int r0 = rbeg + f * 8;
-      const int row = r0 + g;
-      double acc[2] = {0.0, 0.0};
-#pragma unroll 4
-      for (int kk = 0; kk < T_BLK; kk += 4) {
-        const int j = kk + q;
-        double av = (row < n && j < nb) ? trsm_L(t, row, i0 + j) : 0.0;
-        double bv = (j < nb) ? ys[(i0 + j) * T_YP + g] : 0.0;
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                     : "+d"(acc[0]), "+d"(acc[1]) : "d"(av), "d"(bv));
+    for (int fr0 = warp * G; fr0 < nfr; fr0 += (T_THREADS / 32) * G) {
+      double av[G][T_BLK / 4];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int row = rbeg + (fr0 + u) * 8 + g;
+#pragma unroll
+        for (int kk = 0; kk < T_BLK / 4; ++kk) {
+          const int j = 4 * kk + q;
+          av[u][kk] = (fr0 + u < nfr && row < n && j < nb) ? trsm_L(t, row, i0 + j) : 0.0;
+        }
       }
-      if (row < n) {
-        ys[row * T_YP + 2 * q] -= acc[0];
-        ys[row * T_YP + 2 * q + 1] -= acc[1];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        if (fr0 + u >= nfr) break;
+        const int row = rbeg + (fr0 + u) * 8 + g;
+        double acc[NF][2];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < T_BLK / 4; ++kk) {
+          const int j = 4 * kk + q;
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            const double bv = (j < nb) ? ys[(i0 + j) * YP + 8 * f + g] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[f][0]), "+d"(acc[f][1]) : "d"(av[u][kk]), "d"(bv));
+          }
+        }
+        if (row < n) {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            ys[row * YP + 8 * f + 2 * q] -= acc[f][0];
+            ys[row * YP + 8 * f + 2 * q + 1] -= acc[f][1];
+          }
+        }
       }
     }
     __syncthreads();
   }
 
-  for (int idx = tid; idx < n * T_NRHS; idx += T_THREADS) {
-    int c = t.right ? idx % T_NRHS : idx / n;
-    int i = t.right ? idx / T_NRHS : idx % n;
+  for (int idx = tid; idx < n * NR; idx += T_THREADS) {
+    int c = t.right ? idx % NR : idx / n;
+    int i = t.right ? idx / NR : idx % n;
     int col = col0 + c;
-    if (col < t.nrhs) *trsm_Y(t, i, col) = ys[i * T_YP + c];
+    if (col < t.nrhs) *trsm_Y(t, i, col) = ys[i * YP + c];
   }
 }
 

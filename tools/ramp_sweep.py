@@ -17,6 +17,10 @@ call = build_call(kind, m=n, n=n, k=k, tile_size=t, seed=0, alpha=1.0,
                   beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0, uplo="lower",
                   trsm_scaled=True)
 eng = get_engine([0], 8)
+if os.environ.get("BX_TRSM_LEAF"):
+    eng.lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"]))
+if os.environ.get("BX_TRSM_RHS"):
+    eng.lib.bx_set_trsm_rhs(int(os.environ["BX_TRSM_RHS"]))
 for x in [y for y in (call.a, call.b, call.c) if y is not None]:
     eng.register_host(x.matrix.storage)
 

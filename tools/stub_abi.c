@@ -52,6 +52,7 @@ int bx_dev_copy_d2h() { return 0; }
 int bx_dgemm_device() { return 0; }
 int bx_set_gemm_variant() { return 0; }
 int bx_set_trsm_leaf() { return 0; }
+int bx_set_trsm_rhs() { return 0; }
 int bx_set_sgemm_variant() { return 0; }
 int bx_sgemm_device() { return 0; }
 int bx_fp64_peak_probe(int d, int it, double *tf) { *tf = 37.0; return 0; }
