@@ -133,8 +133,15 @@ int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 d
 int bx_set_trsm_leaf(int n);
 /* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16 or 32; default 16) */
 int bx_set_trsm_rhs(int nr);
-/* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile */
+/* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile
+ * (default) */
 int bx_set_sgemm_variant(int variant);
+/* tuning knob: load MN-major SGEMM operands with one 3-d TMA box per stage (1, default) or
+ * one 2-d box per 32-wide group (0) */
+int bx_set_sgemm_mn3d(int on);
+/* diagnostic: SGEMM ablation bits (1 = skip TMA loads after the first ring fill, 2 = skip
+ * the MMAs); results are garbage while set — timing experiments only, default 0 */
+int bx_set_sgemm_debug(int bits);
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha,
                     uint64_t a, int lda, uint64_t b, int ldb, float beta, uint64_t c, int ldc);
 /* register-only DMMA loop: measured FP64 tensor peak for the roofline denominator */

@@ -75,6 +75,8 @@ _SIGS = {
     "bx_set_gemm_variant": [_i],
     "bx_set_trsm_leaf": [_i],
     "bx_set_trsm_rhs": [_i],
+    "bx_set_sgemm_debug": [_i],
+    "bx_set_sgemm_mn3d": [_i],
     "bx_set_sgemm_variant": [_i],
     "bx_last_error": [C.c_char_p, _i],
     "bx_ipc_arena_handle": [_i, _p, _pu64],

@@ -264,7 +264,41 @@ int tensor_map_f32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
   return BX_OK;
 }
 
-int g_sgemm_variant = 0;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile
+// MN-major fp32 operand (rows contiguous, rows % 32 == 0) as a 3-d tensor {32, cols, rows/32}
+// with strides {ld, 32} elements, so ONE box {32, box_k, groups} stages `groups` 32-wide
+// MN groups 4 KB apart — the layout the UMMA MN-major descriptor expects (LBO = 4 KB).
+int tensor_map_f32_mn3d(const float* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_k,
+                        uint32_t groups, CUtensorMap* out) {
+  MapKey key{(uint64_t)base, rows, cols, ld, box_k, groups | 0x10000u, 0xF3u};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) { *out = it->second; return BX_OK; }
+  }
+  if (!g_encode) {
+    CUtensorMap dummy;
+    int rc = tensor_map_f32(base, rows, cols, ld, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, &dummy);
+    if (rc) return rc;
+  }
+  cuuint64_t dims[3] = {32, cols, rows / 32};
+  cuuint64_t strides[2] = {ld * 4, 128};
+  cuuint32_t box[3] = {32, box_k, groups};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(BX_EINVAL, "cuTensorMapEncodeTiled (3-d) failed (" + std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_maps.size() > 65536) g_maps.clear();
+  g_maps[key] = m;
+  *out = m;
+  return BX_OK;
+}
+
+int g_sgemm_variant = 1;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile (default)
+int g_sgemm_mn3d = 1;      // MN-major operands by one 3-d TMA box when the extent allows
+int g_sgemm_debug = 0;     // diagnostic ablation bits (SgemmTask::dbg)
 
 // fp32 task GEMM on tcgen05 (TF32 inputs, fp32 accumulation in TMEM)
 int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
@@ -281,6 +315,9 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
     t.beta = (s0 == 0) ? beta : 1.0f;
     t.mn_lbo = 4096;   // MN-major: 32-wide MN groups (one TMA box) 4 KB apart
     t.mn_sbo = 512;    //           4-row k groups of the 128B_BASE32B atom
+    t.dbg = g_sgemm_debug;
+    t.a3d = g_sgemm_mn3d && !ta && (h % 32) == 0;
+    t.b3d = g_sgemm_mn3d && tb && (w % 32) == 0;
     for (int i = 0; i < n; ++i) {
       const int j = s0 + i, d = depth[j];
       if ((lda[j] & 3) || (ldb[j] & 3) || !aligned16(a[j]) || !aligned16(b[j]))
@@ -289,31 +326,39 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
       int rc;
       // A: untransposed M x K (MN-major boxes 32x32), transposed K x M (K-major box 32 x 128)
       const CUtensorMapSwizzle MN = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, KM = CU_TENSOR_MAP_SWIZZLE_128B;
-      if (!ta) rc = tensor_map_f32(a[j], h, d, lda[j], 32, 32, MN, &t.steps[i].map_a);
+      const uint32_t a_groups = g_sgemm_variant == 1 ? 4u : (uint32_t)(bx::S_BM / 32);
+      const uint32_t b_groups = g_sgemm_variant == 1 ? 4u : (uint32_t)(bx::S_BN / 32);
+      if (!ta && t.a3d) rc = tensor_map_f32_mn3d(a[j], h, d, lda[j], 32, a_groups, &t.steps[i].map_a);
+      else if (!ta) rc = tensor_map_f32(a[j], h, d, lda[j], 32, 32, MN, &t.steps[i].map_a);
       else rc = tensor_map_f32(a[j], d, h, lda[j], bx::S_BK, bx::S_BM, KM, &t.steps[i].map_a);
       if (rc) return rc;
       // B: untransposed K x N (K-major box 32 x BN per CTA), transposed N x K (MN boxes 32x32)
       const uint32_t bn_box = g_sgemm_variant == 1 ? 128u : (uint32_t)bx::S_BN;
       if (!tb) rc = tensor_map_f32(b[j], d, w, ldb[j], bx::S_BK, bn_box, KM, &t.steps[i].map_b);
+      else if (t.b3d) rc = tensor_map_f32_mn3d(b[j], w, d, ldb[j], 32, b_groups, &t.steps[i].map_b);
       else rc = tensor_map_f32(b[j], w, d, ldb[j], 32, 32, MN, &t.steps[i].map_b);
       if (rc) return rc;
     }
     if (g_sgemm_variant == 1) {
-      if (need_attr((const void*)bx::sgemm_tc2_kernel)) {
-        CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::P_SMEM_BYTES));
+      void (*k2)(bx::SgemmTask) = ta ? (tb ? bx::sgemm_tc2_kernel<1, 1> : bx::sgemm_tc2_kernel<1, 0>)
+                                     : (tb ? bx::sgemm_tc2_kernel<0, 1> : bx::sgemm_tc2_kernel<0, 0>);
+      if (need_attr((const void*)k2)) {
+        CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::P_SMEM_BYTES));
       }
       int pairs = ((h + bx::P_BM - 1) / bx::P_BM) * ((w + bx::P_BN - 1) / bx::P_BN);
-      bx::sgemm_tc2_kernel<<<2 * pairs, bx::P_THREADS, bx::P_SMEM_BYTES, s>>>(t);
+      k2<<<2 * pairs, bx::P_THREADS, bx::P_SMEM_BYTES, s>>>(t);
       g_launches++;
       CUDA_TRY(cudaGetLastError());
       if (nsteps <= 0) break;
       continue;
     }
-    if (need_attr((const void*)bx::sgemm_tc_kernel)) {
-      CUDA_TRY(cudaFuncSetAttribute(bx::sgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::S_SMEM_BYTES));
-    }
     int tiles = ((h + bx::S_BM - 1) / bx::S_BM) * ((w + bx::S_BN - 1) / bx::S_BN);
-    bx::sgemm_tc_kernel<<<tiles, bx::S_THREADS, bx::S_SMEM_BYTES, s>>>(t);
+    void (*kern)(bx::SgemmTask) = ta ? (tb ? bx::sgemm_tc_kernel<1, 1> : bx::sgemm_tc_kernel<1, 0>)
+                                     : (tb ? bx::sgemm_tc_kernel<0, 1> : bx::sgemm_tc_kernel<0, 0>);
+    if (need_attr((const void*)kern)) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::S_SMEM_BYTES));
+    }
+    kern<<<tiles, bx::S_THREADS, bx::S_SMEM_BYTES, s>>>(t);
     g_launches++;
     CUDA_TRY(cudaGetLastError());
     if (nsteps <= 0) break;
@@ -1009,6 +1054,16 @@ int bx_set_gemm_variant(int v) {
 int bx_set_sgemm_variant(int v) {
   if (v < 0 || v > 1) return set_err(BX_EINVAL, "sgemm variant must be 0 or 1");
   g_sgemm_variant = v;
+  return BX_OK;
+}
+
+int bx_set_sgemm_mn3d(int on) {
+  g_sgemm_mn3d = on != 0;
+  return BX_OK;
+}
+
+int bx_set_sgemm_debug(int bits) {
+  g_sgemm_debug = bits;
   return BX_OK;
 }
 

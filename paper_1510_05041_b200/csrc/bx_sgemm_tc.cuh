@@ -44,6 +44,10 @@ struct SgemmTask {
   int ta, tb;          // operand stored transposed
   float alpha, beta;
   int mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
+  int dbg;             // diagnostic ablation (bx_set_sgemm_debug): 1 no TMA after the first
+                       // ring fill, 2 no MMA (results are garbage; timing only)
+  int a3d, b3d;        // MN-major operand loaded by ONE 3-d TMA box {32, BK, groups} instead
+                       // of one 2-d box per 32-wide group (extent a multiple of 32)
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -65,6 +69,11 @@ __device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* map, uint
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
       ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
+__device__ __forceinline__ void s_tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n"
+      ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void s_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void s_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -82,7 +91,7 @@ __device__ __forceinline__ uint64_t s_desc(uint32_t saddr, uint32_t lbo, uint32_
 }
 
 // instruction descriptor: D f32, A/B tf32, M=128, N=BN, per-operand major-ness
-__device__ __forceinline__ uint32_t s_idesc(int a_mn_major, int b_mn_major) {
+__host__ __device__ constexpr uint32_t s_idesc(int a_mn_major, int b_mn_major) {
   uint32_t d = 0;
   d |= 1u << 4;                    // c_format F32
   d |= 2u << 7;                    // a_format TF32
@@ -94,6 +103,13 @@ __device__ __forceinline__ uint32_t s_idesc(int a_mn_major, int b_mn_major) {
   return d;
 }
 
+// Operand major-ness is a template parameter (TA: A stored transposed, TB: B stored
+// transposed) so the MMA issue loop is branch-free: its descriptors are the per-kernel
+// base descriptors plus compile-time offsets (stage, k-slice), and the ring is unrolled
+// over the stages.  The single MMA-issuing thread is on the critical path of the tensor
+// pipe (4 MMAs of 128 cycles per stage), so every instruction it spends on address
+// arithmetic is tensor time lost.
+template <int TA, int TB>
 __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_constant__ SgemmTask t) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)s_raw + 1023) & ~(uintptr_t)1023);   // SW128 needs 1 KB
@@ -134,58 +150,87 @@ __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {
       int step = 0, k0 = 0;
+      int dcur = t.nsteps > 0 ? t.steps[0].d : 0;
+      const CUtensorMap* ma = &t.steps[0].map_a;
+      const CUtensorMap* mb = &t.steps[0].map_b;
       for (int it = 0; it < total; ++it) {
         const int st = it % S_STAGES;
         if (it >= S_STAGES) s_mbar_wait(&empty[st], ((it / S_STAGES) - 1) & 1);
         uint8_t* sa = smem + st * S_STAGE_BYTES;
         uint8_t* sb = sa + S_A_BYTES;
-        s_mbar_expect_tx(&full[st], S_STAGE_BYTES);
-        const CUtensorMap* ma = &t.steps[step].map_a;
-        const CUtensorMap* mb = &t.steps[step].map_b;
-        if (t.ta) {
-          // A stored K x M (K contiguous): K-major, one box {BK, BM}
-          s_tma_2d(sa, ma, &full[st], k0, m0);
+        if ((t.dbg & 1) && it >= S_STAGES) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s_u32(&full[st])) : "memory");
         } else {
-          // A stored M x K (M contiguous): MN-major, boxes {32 M, BK} stacked every 4 KB
+          s_mbar_expect_tx(&full[st], S_STAGE_BYTES);
+          if (TA) {
+            // A stored K x M (K contiguous): K-major, one box {BK, BM}
+            s_tma_2d(sa, ma, &full[st], k0, m0);
+          } else {
+            // A stored M x K (M contiguous): MN-major, boxes {32 M, BK} stacked every 4 KB
+            if (t.a3d) {
+              s_tma_3d(sa, ma, &full[st], 0, k0, m0 / 32);
+            } else {
 #pragma unroll
-          for (int i = 0; i < S_BM / 32; ++i) s_tma_2d(sa + i * 4096, ma, &full[st], m0 + 32 * i, k0);
-        }
-        if (!t.tb) {
-          // B stored K x N (K contiguous): K-major, one box {BK, BN}
-          s_tma_2d(sb, mb, &full[st], k0, n0);
-        } else {
+              for (int i = 0; i < S_BM / 32; ++i) s_tma_2d(sa + i * 4096, ma, &full[st], m0 + 32 * i, k0);
+            }
+          }
+          if (!TB) {
+            // B stored K x N (K contiguous): K-major, one box {BK, BN}
+            s_tma_2d(sb, mb, &full[st], k0, n0);
+          } else if (t.b3d) {
+            s_tma_3d(sb, mb, &full[st], 0, k0, n0 / 32);
+          } else {
 #pragma unroll
-          for (int i = 0; i < S_BN / 32; ++i) s_tma_2d(sb + i * 4096, mb, &full[st], n0 + 32 * i, k0);
+            for (int i = 0; i < S_BN / 32; ++i) s_tma_2d(sb + i * 4096, mb, &full[st], n0 + 32 * i, k0);
+          }
         }
         k0 += S_BK;
-        if (k0 >= t.steps[step].d) { k0 = 0; ++step; }
+        if (k0 >= dcur) {
+          k0 = 0;
+          if (++step < t.nsteps) {
+            dcur = t.steps[step].d;
+            ma = &t.steps[step].map_a;
+            mb = &t.steps[step].map_b;
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = s_idesc(!t.ta, t.tb);
-      for (int it = 0; it < total; ++it) {
-        const int st = it % S_STAGES;
-        s_mbar_wait(&full[st], (it / S_STAGES) & 1);
-        s_fence_after();
-        const uint32_t sa = s_u32(smem + st * S_STAGE_BYTES);
-        const uint32_t sb = sa + S_A_BYTES;
+      constexpr uint32_t idesc = s_idesc(!TA, TB);
+      // K-major: the k-slice advances 32 B along the swizzled 128-B row (SBO = 8 rows x
+      // 128 B); MN-major: it advances 8 k-rows (1 KB), SBO = 4 k-rows (512 B) between k
+      // groups, LBO = 4 KB between the 32-wide MN groups (one TMA box each)
+      const uint32_t sbase = s_u32(smem);
+      const uint64_t da0 = TA ? s_desc(sbase, 16, 1024, 2) : s_desc(sbase, t.mn_lbo, t.mn_sbo, 1);
+      const uint64_t db0 = TB ? s_desc(sbase + S_A_BYTES, t.mn_lbo, t.mn_sbo, 1)
+                              : s_desc(sbase + S_A_BYTES, 16, 1024, 2);
+      constexpr uint32_t AK = TA ? 32 / 16 : 1024 / 16;     // descriptor units (16 B)
+      constexpr uint32_t BKS = TB ? 1024 / 16 : 32 / 16;
+      constexpr uint32_t SU = S_STAGE_BYTES / 16;
+      const bool do_mma = !(t.dbg & 2);
+      for (int it0 = 0; it0 < total; it0 += S_STAGES) {
+        const uint32_t par = (it0 / S_STAGES) & 1;
 #pragma unroll
-        for (int kk = 0; kk < S_BK / 8; ++kk) {
-          // K-major: advance 32 B along the swizzled 128-B row; SBO = 8 rows x 128 B.
-          // MN-major: advance 8 k-rows (1 KB); SBO = 4 k-rows (512 B) between k groups,
-          // LBO = 4 KB between the 32-wide MN groups (one TMA box each).
-          const uint64_t da = t.ta ? s_desc(sa + kk * 32, 16, 1024, 2) : s_desc(sa + kk * 1024, t.mn_lbo, t.mn_sbo, 1);
-          const uint64_t db = t.tb ? s_desc(sb + kk * 1024, t.mn_lbo, t.mn_sbo, 1) : s_desc(sb + kk * 32, 16, 1024, 2);
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
-              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        for (int st = 0; st < S_STAGES; ++st) {
+          if (it0 + st >= total) break;
+          s_mbar_wait(&full[st], par);
+          s_fence_after();
+          if (do_mma) {
+#pragma unroll
+            for (int kk = 0; kk < S_BK / 8; ++kk) {
+              const uint32_t acc = (it0 + st + kk) != 0;
+              asm volatile(
+                  "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                  " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                  ::"r"(tmem), "l"(da0 + (uint64_t)(st * SU + kk * AK)), "l"(db0 + (uint64_t)(st * SU + kk * BKS)),
+                    "n"(idesc), "r"(acc));
+            }
+          }
+          // frees the stage once these MMAs have read it
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                       ::"r"(s_u32(&empty[st])) : "memory");
         }
-        // frees the stage once these MMAs have read it
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                     ::"r"(s_u32(&empty[st])) : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                    ::"r"(s_u32(accum)) : "memory");
@@ -212,7 +257,7 @@ __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_con
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0u;
       }
-      if (row < t.h) {
+      if (row < t.h && !(t.dbg & 8)) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int col = n0 + c0 + i;
@@ -276,6 +321,13 @@ __device__ __forceinline__ void p_tma_2d_pair(void* dst, const CUtensorMap* map,
       ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar) & PEER_MASK), "r"(c0), "r"(c1) : "memory");
 }
 
+__device__ __forceinline__ void p_tma_3d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n"
+      ::"r"(s_u32(dst)), "l"((uint64_t)map), "r"(s_u32(bar) & PEER_MASK), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+template <int TA, int TB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     sgemm_tc2_kernel(const __grid_constant__ SgemmTask t) {
   extern __shared__ __align__(1024) uint8_t s_raw[];
@@ -318,6 +370,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int step = 0, k0 = 0;
+      int dcur = t.nsteps > 0 ? t.steps[0].d : 0;
+      const CUtensorMap* ma = &t.steps[0].map_a;
+      const CUtensorMap* mb = &t.steps[0].map_b;
       for (int it = 0; it < total; ++it) {
         const int st = it % P_STAGES;
         if (it >= P_STAGES) p_mbar_wait(&empty[st], ((it / P_STAGES) - 1) & 1);
@@ -325,46 +380,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         uint8_t* sb = sa + P_A_BYTES;
         // the leader's barrier expects both CTAs' bytes
         if (rank == 0) s_mbar_expect_tx(&full[st], 2 * P_STAGE_BYTES);
-        const CUtensorMap* ma = &t.steps[step].map_a;
-        const CUtensorMap* mb = &t.steps[step].map_b;
-        if (t.ta) {
+        if (TA) {
           p_tma_2d_pair(sa, ma, &full[st], k0, my_m0);
+        } else if (t.a3d) {
+          p_tma_3d_pair(sa, ma, &full[st], 0, k0, my_m0 / 32);
         } else {
 #pragma unroll
           for (int i = 0; i < 4; ++i) p_tma_2d_pair(sa + i * 4096, ma, &full[st], my_m0 + 32 * i, k0);
         }
-        if (!t.tb) {
+        if (!TB) {
           p_tma_2d_pair(sb, mb, &full[st], k0, my_n0);
+        } else if (t.b3d) {
+          p_tma_3d_pair(sb, mb, &full[st], 0, k0, my_n0 / 32);
         } else {
 #pragma unroll
           for (int i = 0; i < 4; ++i) p_tma_2d_pair(sb + i * 4096, mb, &full[st], my_n0 + 32 * i, k0);
         }
         k0 += P_BK;
-        if (k0 >= t.steps[step].d) { k0 = 0; ++step; }
+        if (k0 >= dcur) {
+          k0 = 0;
+          if (++step < t.nsteps) {
+            dcur = t.steps[step].d;
+            ma = &t.steps[step].map_a;
+            mb = &t.steps[step].map_b;
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      uint32_t idesc = s_idesc(!t.ta, t.tb);
-      idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(P_BM >> 4) << 24);   // M = 256
-      for (int it = 0; it < total; ++it) {
-        const int st = it % P_STAGES;
-        p_mbar_wait(&full[st], (it / P_STAGES) & 1);
-        s_fence_after();
-        const uint32_t sa = s_u32(smem + st * P_STAGE_BYTES);
-        const uint32_t sb = sa + P_A_BYTES;
+      constexpr uint32_t idesc = (s_idesc(!TA, TB) & ~(0x1Fu << 24)) | ((uint32_t)(P_BM >> 4) << 24);  // M = 256
+      const uint32_t sbase = s_u32(smem);
+      const uint64_t da0 = TA ? s_desc(sbase, 16, 1024, 2) : s_desc(sbase, t.mn_lbo, t.mn_sbo, 1);
+      const uint64_t db0 = TB ? s_desc(sbase + P_A_BYTES, t.mn_lbo, t.mn_sbo, 1)
+                              : s_desc(sbase + P_A_BYTES, 16, 1024, 2);
+      constexpr uint32_t AK = TA ? 32 / 16 : 1024 / 16;
+      constexpr uint32_t BKS = TB ? 1024 / 16 : 32 / 16;
+      constexpr uint32_t SU = P_STAGE_BYTES / 16;
+      for (int it0 = 0; it0 < total; it0 += P_STAGES) {
+        const uint32_t par = (it0 / P_STAGES) & 1;
 #pragma unroll
-        for (int kk = 0; kk < P_BK / 8; ++kk) {
-          const uint64_t da = t.ta ? s_desc(sa + kk * 32, 16, 1024, 2) : s_desc(sa + kk * 1024, t.mn_lbo, t.mn_sbo, 1);
-          const uint64_t db = t.tb ? s_desc(sb + kk * 1024, t.mn_lbo, t.mn_sbo, 1) : s_desc(sb + kk * 32, 16, 1024, 2);
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
-              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        for (int st = 0; st < P_STAGES; ++st) {
+          if (it0 + st >= total) break;
+          p_mbar_wait(&full[st], par);
+          s_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < P_BK / 8; ++kk) {
+            const uint32_t acc = (it0 + st + kk) != 0;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                ::"r"(tmem), "l"(da0 + (uint64_t)(st * SU + kk * AK)), "l"(db0 + (uint64_t)(st * SU + kk * BKS)),
+                  "n"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                       ::"r"(s_u32(&empty[st])), "h"((uint16_t)3) : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-                     ::"r"(s_u32(&empty[st])), "h"((uint16_t)3) : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
                    ::"r"(s_u32(accum)), "h"((uint16_t)3) : "memory");

@@ -207,11 +207,28 @@ def test_concurrent_mode_and_trace():
     assert all(e.time_end >= e.time_start for e in ks)
 
 
+@pytest.mark.parametrize("variant,mn3d,shape", [(1, 1, (1500, 1300, 1100)), (0, 1, (1500, 1300, 1100)),
+                                                (1, 1, (1536, 1280, 1024)), (0, 1, (1536, 1280, 1024)),
+                                                (1, 0, (1536, 1280, 1024))])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
-def test_sgemm_tcgen05_against_fp64_oracle(ta, tb):
+def test_sgemm_tcgen05_against_fp64_oracle(ta, tb, variant, mn3d, shape):
     """SGEMM has no reference path (tiling.py:57-60 is float64 only): compare with the
-    float64 tiled oracle on the same float32-representable inputs, eps = 2^-23."""
-    call = build_call("gemm", m=1500, n=1300, k=1100, tile_size=512, seed=11, alpha=1.0, beta=0.5,
+    float64 tiled oracle on the same float32-representable inputs, eps = 2^-23.  Both
+    kernels (1-SM 128x256, 2-SM cta_group::2 256x256), MN-major operands by 3-d or 2-d TMA
+    boxes, ragged (1500x1300x1100) and 32-aligned shapes."""
+    from paper_1510_05041_b200 import _native
+    lib = _native.load()
+    lib.bx_set_sgemm_variant(variant)
+    lib.bx_set_sgemm_mn3d(mn3d)
+    try:
+        _sgemm_case(ta, tb, *shape)
+    finally:
+        lib.bx_set_sgemm_variant(1)
+        lib.bx_set_sgemm_mn3d(1)
+
+
+def _sgemm_case(ta, tb, m, n, k):
+    call = build_call("gemm", m=m, n=n, k=k, tile_size=512, seed=11, alpha=1.0, beta=0.5,
                       trans_a=ta, trans_b=tb, dtype=np.float32)
     a = call.a.matrix.as_2d().astype(np.float64)
     b = call.b.matrix.as_2d().astype(np.float64)
@@ -220,7 +237,7 @@ def test_sgemm_tcgen05_against_fp64_oracle(ta, tb):
     out = call.c.matrix.as_2d().astype(np.float64)
     ref = c0.copy()
     tiled.run_tiled("gemm", a, ref, b, tile_size=512, alpha=1.0, beta=0.5, trans_a=ta, trans_b=tb)
-    r = tolerance.gemm_ratio(out, ref, a_norm=np.linalg.norm(a), b_norm=np.linalg.norm(b), k=1100,
+    r = tolerance.gemm_ratio(out, ref, a_norm=np.linalg.norm(a), b_norm=np.linalg.norm(b), k=k,
                              alpha=1.0, beta=0.5, c0_norm=np.linalg.norm(c0),
                              eps=float(np.finfo(np.float32).eps))
     assert r <= tolerance.BOUND, r
