@@ -391,7 +391,7 @@ def result_line(args, cfg, val, e2e, peak_measured, clk, cpu, f32, execution="si
                                         "h2d_gbs_assumed": h2d_bw / 1e9, "p2p_gbs_assumed": p2p_bw / 1e9}},
         "roofline": {"bound": "tensor", "achieved": kernel_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": kernel_tf / peak_tf, "traffic": None if f32 else traffic,
-                     "kernel": ("bx::sgemm_tc_kernel (tcgen05.mma kind::tf32, TMEM accumulators, TMA)"
+                     "kernel": ("bx::sgemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 pair tile, TMEM accumulators, TMA)"
                                 if f32 else "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
                      "peak_source": peak_src,
                      "fp64_dmma_peak_measured": peak_measured,
