@@ -90,6 +90,26 @@ __global__ void __launch_bounds__(T_THREADS) trsm_panel_kernel(const __grid_cons
       ls[(idx / T_BLK) * (T_BLK + 1) + idx % T_BLK] = v[u];
     }
     __syncthreads();
+    // Trailing-update operands L(r, i0:i0+nb) do not depend on Y: the first chunk's loads
+    // are issued now and land while the substitution below runs.  Row fragments (8 rows)
+    // go to warps round-robin, U per warp per chunk, so every warp has work.
+    constexpr int U = 4;
+    const int rbeg = i0 + nb;
+    const int nfr = (n - rbeg + 7) / 8;
+    double av[U][T_BLK / 4];
+    auto load_frags = [&](int c) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int fr = warp + 8 * (c * U + u);
+        const int row = rbeg + fr * 8 + g;
+#pragma unroll
+        for (int kk = 0; kk < T_BLK / 4; ++kk) {
+          const int j = 4 * kk + q;
+          av[u][kk] = (fr < nfr && row < n && j < nb) ? trsm_L(t, row, i0 + j) : 0.0;
+        }
+      }
+    };
+    load_frags(0);
     {
       // substitution on the diagonal block: warp -> RHS (NR / 8 each), lane -> row; the
       // reference divides by the diagonal (kernels.py:140-159), so do we
@@ -118,27 +138,15 @@ __global__ void __launch_bounds__(T_THREADS) trsm_panel_kernel(const __grid_cons
     }
     __syncthreads();
     if (i0 + T_BLK < n) load_diag(i0 + T_BLK);
-    // trailing update: Y[r] -= L(r, i0:i0+nb) * Y(i0:i0+nb) for r >= i0+nb (DMMA m8n8k4).
-    // A warp takes its row fragments G at a time and issues all their L loads before the
-    // first DMMA (one L2 round trip per G fragments); one L fragment feeds NF DMMAs.
-    constexpr int G = 4;
-    const int rbeg = i0 + nb;
-    const int nfr = (n - rbeg + 7) / 8;
-    for (int fr0 = warp * G; fr0 < nfr; fr0 += (T_THREADS / 32) * G) {
-      double av[G][T_BLK / 4];
+    // trailing update: Y[r] -= L(r, i0:i0+nb) * Y(i0:i0+nb) for r >= i0+nb (DMMA m8n8k4);
+    // one L fragment feeds NF DMMAs, U fragments give 2*U*NF independent accumulators
+    for (int c = 0; 8 * c * U < nfr; ++c) {
+      if (c > 0) load_frags(c);
 #pragma unroll
-      for (int u = 0; u < G; ++u) {
-        const int row = rbeg + (fr0 + u) * 8 + g;
-#pragma unroll
-        for (int kk = 0; kk < T_BLK / 4; ++kk) {
-          const int j = 4 * kk + q;
-          av[u][kk] = (fr0 + u < nfr && row < n && j < nb) ? trsm_L(t, row, i0 + j) : 0.0;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        if (fr0 + u >= nfr) break;
-        const int row = rbeg + (fr0 + u) * 8 + g;
+      for (int u = 0; u < U; ++u) {
+        const int fr = warp + 8 * (c * U + u);
+        if (fr >= nfr) break;
+        const int row = rbeg + fr * 8 + g;
         double acc[NF][2];
 #pragma unroll
         for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
