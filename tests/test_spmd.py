@@ -47,9 +47,9 @@ def test_spmd_gemm_three_ranks_host_bytes_once():
     _check(outs, 3)
     o = outs[0]
     # first-holder policy: each input tile crosses the host link once (A + B + C move-in)
-    assert o["h2d"] == (256 * 256 * 3) * 8
-    assert o["host"] == 2 * 16
-    assert o["second_tasks"] == o["n_tasks"]
+    assert o["h2d"] == (256 * 256 * 3) * 8, outs
+    assert o["host"] == 2 * 16, outs
+    assert o["second_tasks"] == o["n_tasks"], outs
 
 
 def test_spmd_trsm_three_ranks_small_station():
