@@ -59,3 +59,14 @@ int bx_set_sgemm_variant() { return 0; }
 int bx_sgemm_device() { return 0; }
 int bx_fp64_peak_probe(int d, int it, double *tf) { *tf = 37.0; return 0; }
 int bx_last_error(char *buf, int len) { if (len) buf[0] = 0; return 0; }
+/* one process per GPU (spmd.py) */
+int bx_ipc_arena_handle(int d, void *h, uint64_t *b) { *b = 0; return 0; }
+int bx_ipc_open(int d, const void *h, uint64_t *b) { *b = 0; return 0; }
+int bx_ipc_close(int d, uint64_t b) { return 0; }
+int bx_host_register_mapped(void *p, uint64_t n, uint64_t *dp) { *dp = (uint64_t)p; return 0; }
+int bx_copy_remote(int d, uint64_t o, uint64_t s, uint64_t n, uint64_t f, uint32_t m, int nw, const int *w,
+                   int *ev) { return EV(ev); }
+int bx_write_flag(int d, int l, uint64_t f, uint32_t v, int nw, const int *w) { return 0; }
+int bx_atomic_add(int64_t *p, int64_t v, int64_t *old) { *old = __atomic_fetch_add(p, v, __ATOMIC_SEQ_CST); return 0; }
+int bx_atomic_cas(int64_t *p, int64_t e, int64_t d, int64_t *old) {
+  int64_t x = e; __atomic_compare_exchange_n(p, &x, d, 0, __ATOMIC_SEQ_CST, __ATOMIC_SEQ_CST); *old = x; return 0; }
