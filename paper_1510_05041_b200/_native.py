@@ -113,6 +113,12 @@ def load(path: str = _LIB_PATH):
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        # kernel-variant knobs from the environment (tuning runs / variant test sweeps)
+        for env, fn in (("BX_GEMM_VARIANT", "bx_set_gemm_variant"),
+                        ("BX_SGEMM_VARIANT", "bx_set_sgemm_variant"),
+                        ("BX_TRSM_LEAF", "bx_set_trsm_leaf"), ("BX_TRSM_RHS", "bx_set_trsm_rhs")):
+            if os.environ.get(env):
+                getattr(lib, fn)(int(os.environ[env]))
         _lib = lib
         return lib
 

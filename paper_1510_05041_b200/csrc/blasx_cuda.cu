@@ -233,9 +233,15 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 // 2-d fp32 column-major matrix (rows contiguous, leading dimension ld elements) -> tensor
 // map with a {box0 (rows), box1 (cols)} box, 128-B swizzle, zero fill out of bounds.
+int tensor_map_2d(const void* base, bool f64, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
+                  uint32_t box1, CUtensorMapSwizzle swz, CUtensorMap* out);
 int tensor_map_f32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0, uint32_t box1,
                    CUtensorMapSwizzle swz, CUtensorMap* out) {
-  MapKey key{(uint64_t)base, rows, cols, ld, box0, box1, (uint32_t)swz};
+  return tensor_map_2d(base, false, rows, cols, ld, box0, box1, swz, out);
+}
+int tensor_map_2d(const void* base, bool f64, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
+                  uint32_t box1, CUtensorMapSwizzle swz, CUtensorMap* out) {
+  MapKey key{(uint64_t)base, rows, cols, ld, box0, box1, (uint32_t)swz | (f64 ? 0x100u : 0u)};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_maps.find(key);
@@ -249,11 +255,12 @@ int tensor_map_f32(const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
     g_encode = (PFN_encodeTiled)fn;
   }
   cuuint64_t dims[2] = {rows, cols};
-  cuuint64_t strides[1] = {ld * 4};
+  cuuint64_t strides[1] = {ld * (f64 ? 8 : 4)};
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t estr[2] = {1, 1};
   CUtensorMap m;
-  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+  CUresult r = g_encode(&m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base,
+                        dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(BX_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -368,6 +375,43 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
 
 // General gemm over raw pointers, splitting step lists longer than G_MAX_STEPS into
 // several launches (later launches accumulate with beta = 1).
+// FP64 task GEMM fed by TMA (bx::gemm_task_tma_kernel): tensor maps per step operand,
+// cached by (pointer, extents, ld); steps beyond T_MAX_STEPS go to further launches.
+int gemm_tma(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, const double* const* a,
+             const int* lda, const double* const* b, const int* ldb, const int* depth, double alpha,
+             double beta, double* c, int ldc) {
+  const CUtensorMapSwizzle SW = CU_TENSOR_MAP_SWIZZLE_128B;
+  for (int s0 = 0; s0 < nsteps; s0 += bx::T_MAX_STEPS) {
+    bx::GemmTmaTask t;
+    memset(&t, 0, sizeof(t));
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = 8;
+    t.alpha = alpha;
+    t.beta = (s0 == 0) ? beta : 1.0;
+    const int n = nsteps - s0 < bx::T_MAX_STEPS ? nsteps - s0 : bx::T_MAX_STEPS;
+    t.nsteps = n;
+    for (int i = 0; i < n; ++i) {
+      const int j = s0 + i, d = depth[j];
+      t.steps[i].d = d;
+      int rc = ta ? tensor_map_2d(a[j], true, d, h, lda[j], bx::T_BK, bx::T_BM, SW, &t.steps[i].ma)
+                  : tensor_map_2d(a[j], true, h, d, lda[j], 16, bx::T_BK, SW, &t.steps[i].ma);
+      if (rc) return rc;
+      rc = tb ? tensor_map_2d(b[j], true, w, d, ldb[j], 16, bx::T_BK, SW, &t.steps[i].mb)
+              : tensor_map_2d(b[j], true, d, w, ldb[j], bx::T_BK, bx::T_BN, SW, &t.steps[i].mb);
+      if (rc) return rc;
+    }
+    void (*k)(bx::GemmTmaTask) = ta ? (tb ? bx::gemm_task_tma_kernel<true, true> : bx::gemm_task_tma_kernel<true, false>)
+                                    : (tb ? bx::gemm_task_tma_kernel<false, true> : bx::gemm_task_tma_kernel<false, false>);
+    if (need_attr((const void*)k)) {
+      CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::T_SMEM_BYTES));
+    }
+    const int tiles = ((h + bx::T_BM - 1) / bx::T_BM) * ((w + bx::T_BN - 1) / bx::T_BN);
+    k<<<tiles, bx::T_THREADS_G, bx::T_SMEM_BYTES, s>>>(t);
+    g_launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return BX_OK;
+}
+
 int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, const double* const* a,
              const int* lda, const double* const* b, const int* ldb, const int* depth, double alpha,
              double beta, double* c, int ldc) {
@@ -388,6 +432,7 @@ int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
     t.alpha = alpha; t.beta = beta;
     return launch_gemm(ta, tb, t, s);
   }
+  if (g_gemm_variant == 8) return gemm_tma(s, ta, tb, tri, h, w, nsteps, a, lda, b, ldb, depth, alpha, beta, c, ldc);
   for (int s0 = 0; s0 < nsteps; s0 += bx::G_MAX_STEPS) {
     bx::GemmTask t{};
     t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = 8;

@@ -443,3 +443,198 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
 }
 
 }  // namespace bx
+
+// ---------------------------------------------------------------------------------------
+// TMA-fed variant of the FP64 task GEMM (bx_set_gemm_variant(8)).  Same task contract and
+// tile shape (CTA 128x128x16, 8 warps of 64x32, DMMA m8n8k4), but the operand slabs are
+// staged by the tensor-memory accelerator: one thread issues the bulk tensor copies of a
+// stage (128-B swizzled boxes, zero fill past every tile edge, bytes complete on the
+// stage's mbarrier), so the other 255 threads spend no issue slots on loads — in the
+// cp.async kernel above every thread issues 4 copies, their address arithmetic and an
+// arrive per slab.  Fragment loads undo the 128-B swizzle (16-B chunk ^ row % 8).
+// ---------------------------------------------------------------------------------------
+#include <cuda.h>
+namespace bx {
+
+constexpr int T_MAX_STEPS = 16, T_STAGES = 6, T_DIST = 4;
+constexpr int T_BM = 128, T_BN = 128, T_BK = 16, T_WM = 64, T_WN = 32, T_THREADS_G = 256;
+constexpr int T_A_BYTES = T_BM * T_BK * 8, T_B_BYTES = T_BN * T_BK * 8;   // 16 KB each
+constexpr int T_STAGE_BYTES = T_A_BYTES + T_B_BYTES;
+constexpr int T_SMEM_BYTES = T_STAGES * T_STAGE_BYTES + 1024 + 2 * T_STAGES * 8;
+
+struct GemmTmaStep {
+  CUtensorMap ma;      // A_s: MN-major boxes {16 m, 16 k} or K-major box {16 k, 128 m}
+  CUtensorMap mb;      // B_s: K-major box {16 k, 128 n} or MN-major boxes {16 n, 16 k}
+  int d;
+  int pad_[31];
+};
+
+struct GemmTmaTask {
+  GemmTmaStep steps[T_MAX_STEPS];
+  double* c;
+  int ldc, h, w, nsteps, tri, group_m;
+  double alpha, beta;
+};
+
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      ::"r"(dst), "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(T_THREADS_G, 1) gemm_task_tma_kernel(const __grid_constant__ GemmTmaTask t) {
+  extern __shared__ __align__(1024) uint8_t t_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)t_raw + 1023) & ~(uintptr_t)1023);   // 128-B swizzle atoms
+  uint64_t* full = (uint64_t*)(smem + T_STAGES * T_STAGE_BYTES);
+  uint64_t* empty = full + T_STAGES;
+  constexpr int MF = T_WM / 8, NF = T_WN / 8, KQ = T_BK / 4, WARPS = T_THREADS_G / 32;
+  constexpr int WARPS_M = T_BM / T_WM;
+
+  const int tiles_m = (t.h + T_BM - 1) / T_BM, tiles_n = (t.w + T_BN - 1) / T_BN;
+  const int bid = blockIdx.x;
+  const int per_group = t.group_m * tiles_n;
+  const int first_m = (bid / per_group) * t.group_m;
+  const int gsize = min(tiles_m - first_m, t.group_m);
+  const int m0 = (first_m + (bid % per_group) % gsize) * T_BM;
+  const int n0 = ((bid % per_group) / gsize) * T_BN;
+  if (t.tri == TRI_LOWER && n0 >= m0 + T_BM) return;
+  if (t.tri == TRI_UPPER && m0 >= n0 + T_BN) return;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int total = 0;
+  for (int s = 0; s < t.nsteps; ++s) total += (t.steps[s].d + T_BK - 1) / T_BK;
+  if (tid == 0) {
+    for (int s = 0; s < T_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t sbase = smem_u32(smem);
+  int ld_step = 0, ld_k = 0, ld_d = t.nsteps > 0 ? t.steps[0].d : 0;
+  auto produce = [&](int slab) {
+    const int stage = slab % T_STAGES;
+    if (slab >= T_STAGES) mbar_wait(&empty[stage], ((slab / T_STAGES) - 1) & 1);
+    const uint32_t sa = sbase + stage * T_STAGE_BYTES, sb = sa + T_A_BYTES;
+    const uint32_t bar = smem_u32(&full[stage]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(T_STAGE_BYTES) : "memory");
+    const GemmTmaStep& st = t.steps[ld_step];
+    if (TA) {
+      tma2d(sa, &st.ma, bar, ld_k, m0);                    // A stored K x M: one K-major box
+    } else {
+#pragma unroll
+      for (int g = 0; g < T_BM / 16; ++g) tma2d(sa + g * 2048, &st.ma, bar, m0 + 16 * g, ld_k);
+    }
+    if (!TB) {
+      tma2d(sb, &st.mb, bar, ld_k, n0);                    // B stored K x N: one K-major box
+    } else {
+#pragma unroll
+      for (int g = 0; g < T_BN / 16; ++g) tma2d(sb + g * 2048, &st.mb, bar, n0 + 16 * g, ld_k);
+    }
+    ld_k += T_BK;
+    if (ld_k >= ld_d) {
+      ld_k = 0;
+      if (++ld_step < t.nsteps) ld_d = t.steps[ld_step].d;
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < T_DIST && s < total; ++s) produce(s);
+
+  const int wm = (warp % WARPS_M) * T_WM, wn = (warp / WARPS_M) * T_WN;
+  const int g = lane >> 2, q = lane & 3;
+  // per-lane swizzled byte offsets of the fragment loads (see the layout notes above)
+  //   K-major  (row = mn, 16-B chunk = k/2):   mn*128 + ((k/2) ^ (mn%8))*16 + (k%2)*8
+  //   MN-major (box per 16 mn, row = k):       (mn/16)*2048 + k*128 + (((mn%16)/2) ^ (k%8))*16 + (mn%2)*8
+  uint32_t kmaj[KQ], mnmaj[4];
+#pragma unroll
+  for (int kq = 0; kq < KQ; ++kq) kmaj[kq] = (((2 * kq + (q >> 1)) ^ g) << 4) + (q & 1) * 8;
+#pragma unroll
+  for (int ih = 0; ih < 2; ++ih)
+#pragma unroll
+    for (int kh = 0; kh < 2; ++kh)
+      mnmaj[ih * 2 + kh] = ((((ih * 4 + (g >> 1)) ^ (kh * 4 + q)) << 4) + (g & 1) * 8 + q * 128);
+  auto fa = [&](const uint8_t* a, int i, int kq) -> double {
+    const int mn = wm + i * 8;
+    if (TA) return *(const double*)(a + (mn + g) * 128 + kmaj[kq]);
+    return *(const double*)(a + (mn >> 4) * 2048 + kq * 512 + mnmaj[(i & 1) * 2 + (kq & 1)]);
+  };
+  auto fb = [&](const uint8_t* b, int j, int kq) -> double {
+    const int mn = wn + j * 8;
+    if (!TB) return *(const double*)(b + (mn + g) * 128 + kmaj[kq]);
+    return *(const double*)(b + (mn >> 4) * 2048 + kq * 512 + mnmaj[(j & 1) * 2 + (kq & 1)]);
+  };
+
+  double acc[MF][NF][2];
+#pragma unroll
+  for (int i = 0; i < MF; ++i)
+#pragma unroll
+    for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[2][MF], rb[2][NF];
+  if (total > 0) {
+    mbar_wait(&full[0], 0);
+#pragma unroll
+    for (int i = 0; i < MF; ++i) ra[0][i] = fa(smem, i, 0);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) rb[0][j] = fb(smem + T_A_BYTES, j, 0);
+  }
+  for (int it = 0; it < total; ++it) {
+    if (tid == 0 && it + T_DIST < total) produce(it + T_DIST);
+    const int stage = it % T_STAGES;
+    const uint8_t* a = smem + stage * T_STAGE_BYTES;
+    const uint8_t* b = a + T_A_BYTES;
+#pragma unroll
+    for (int kq = 0; kq < KQ; ++kq) {
+      const int cur = kq & 1, nx = cur ^ 1;
+      if (kq + 1 < KQ) {
+#pragma unroll
+        for (int i = 0; i < MF; ++i) ra[nx][i] = fa(a, i, kq + 1);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) rb[nx][j] = fb(b, j, kq + 1);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);   // this warp is done reading the stage
+        if (it + 1 < total) {
+          const int ns = (it + 1) % T_STAGES;
+          mbar_wait(&full[ns], ((it + 1) / T_STAGES) & 1);
+          const uint8_t* a2 = smem + ns * T_STAGE_BYTES;
+          const uint8_t* b2 = a2 + T_A_BYTES;
+#pragma unroll
+          for (int i = 0; i < MF; ++i) ra[nx][i] = fa(a2, i, 0);
+#pragma unroll
+          for (int j = 0; j < NF; ++j) rb[nx][j] = fb(b2, j, 0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NF; ++jj) {
+          const int j = (i & 1) ? NF - 1 - jj : jj;
+          dmma(acc[i][j], ra[cur][i], rb[cur][j]);
+        }
+    }
+  }
+
+  const double alpha = t.alpha, beta = t.beta;
+#pragma unroll
+  for (int i = 0; i < MF; ++i) {
+    const int r = m0 + wm + i * 8 + g;
+    if (r >= t.h) continue;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = n0 + wn + j * 8 + 2 * q + e;
+        if (cc >= t.w) continue;
+        if (t.tri == TRI_LOWER && cc > r) continue;
+        if (t.tri == TRI_UPPER && cc < r) continue;
+        double* p = t.c + (size_t)cc * t.ldc + r;
+        double v = alpha * acc[i][j][e];
+        if (beta != 0.0) v = fma(beta, *p, v);
+        *p = v;
+      }
+    }
+  }
+}
+
+}  // namespace bx
