@@ -90,6 +90,12 @@ int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int
 int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps, const uint64_t* a_off,
                   const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, float alpha,
                   float beta, uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out);
+/* the same task GEMM (f32 = 0: bx_gemm_task, 1: bx_sgemm_task) with the steps packed as
+ * nsteps rows of 5 int64 {a_off, lda, b_off, ldb, depth}: one host array per launch (the
+ * runtime's issue path marshals one buffer instead of five) */
+int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
+                        const int64_t* steps, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
+                        const int* wait, int* ev_out);
 /* in-place triangular solve of B (h x w) against the diagonal tile A */
 int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h,
                  int w, double alpha, uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait,

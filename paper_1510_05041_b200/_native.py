@@ -50,6 +50,7 @@ _SIGS = {
                      _u64, _i, _i, _pi, _pi],
     "bx_sgemm_task": [_i, _i, _i, _i, _i, _i, _i, _pu64, _pi, _pu64, _pi, _pi, C.c_float, C.c_float,
                       _u64, _i, _i, _pi, _pi],
+    "bx_gemm_task_packed": [_i, _i, _i, _i, _i, _i, _i, _i, _i, _p, _d, _d, _u64, _i, _i, _pi, _pi],
     "bx_sgemm_device": [_i, _i, _i, _i, _i, _i, _i, C.c_float, _u64, _i, _u64, _i, C.c_float, _u64, _i],
     "bx_trsm_tile": [_i, _i, _i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_materialize": [_i, _i, _i, _i, _i, _i, _i, _u64, _i, _u64, _i, _i, _pi, _pi],

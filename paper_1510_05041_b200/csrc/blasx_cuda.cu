@@ -846,6 +846,26 @@ int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps,
   return finish(dev, s, ev_out);
 }
 
+int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
+                        const int64_t* steps, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
+                        const int* wait, int* ev_out) {
+  if (nsteps < 0 || nsteps > 4096) return set_err(BX_EINVAL, "gemm: bad step count");
+  std::vector<uint64_t> ao(nsteps > 0 ? nsteps : 1), bo(nsteps > 0 ? nsteps : 1);
+  std::vector<int> la(nsteps > 0 ? nsteps : 1), lb(nsteps > 0 ? nsteps : 1), dp(nsteps > 0 ? nsteps : 1);
+  for (int i = 0; i < nsteps; ++i) {
+    const int64_t* r = steps + 5 * i;
+    if (r[0] < 0 || r[2] < 0) return set_err(BX_EINVAL, "gemm: negative operand offset");
+    ao[i] = (uint64_t)r[0]; la[i] = (int)r[1]; bo[i] = (uint64_t)r[2]; lb[i] = (int)r[3]; dp[i] = (int)r[4];
+  }
+  if (f32) {
+    if (tri) return set_err(BX_EINVAL, "sgemm: no triangle mode");
+    return bx_sgemm_task(dev, stream, ta, tb, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(), dp.data(),
+                         (float)alpha, (float)beta, c_off, ldc, n_wait, wait, ev_out);
+  }
+  return bx_gemm_task(dev, stream, ta, tb, tri, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(), dp.data(),
+                      alpha, beta, c_off, ldc, n_wait, wait, ev_out);
+}
+
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha, uint64_t a, int lda,
                     uint64_t b, int ldb, float beta, uint64_t c, int ldc) {
   Device* D = dev_of(dev);

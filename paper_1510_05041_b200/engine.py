@@ -9,6 +9,7 @@ CPU implementation of any of these operations.
 from __future__ import annotations
 
 import ctypes as C
+from array import array
 import threading
 
 from . import _native as N
@@ -162,25 +163,21 @@ class CudaEngine:
 
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
              f32=False) -> int:
-        """One task GEMM launch; ``f32`` selects the tcgen05 TF32 kernel (SGEMM)."""
+        """One task GEMM launch; ``f32`` selects the tcgen05 TF32 kernel (SGEMM).  ``steps``
+        = [(a_off, lda, b_off, ldb, depth), ...], marshalled as one packed int64 array."""
         n = len(steps)
-        a_off = (C.c_uint64 * n)(*[s[0] for s in steps])
-        lda = (C.c_int * n)(*[s[1] for s in steps])
-        b_off = (C.c_uint64 * n)(*[s[2] for s in steps])
-        ldb = (C.c_int * n)(*[s[3] for s in steps])
-        dep = (C.c_int * n)(*[s[4] for s in steps])
+        if f32 and tri:
+            raise ValueError("the fp32 task GEMM has no triangle mode")
+        flat = array("q", [v for st in steps for v in st])
         ev = C.c_int(-1)
-        nw, wp = self._waits(waits)
-        if f32:
-            if tri:
-                raise ValueError("the fp32 task GEMM has no triangle mode")
-            N.check(self.lib.bx_sgemm_task(slot, stream, int(ta), int(tb), h, w, n, a_off, lda,
-                                           b_off, ldb, dep, float(alpha), float(beta), c_off, ldc,
-                                           nw, wp, C.byref(ev)), "sgemm task")
-            return ev.value
-        N.check(self.lib.bx_gemm_task(slot, stream, int(ta), int(tb), tri, h, w, n, a_off, lda,
-                                      b_off, ldb, dep, float(alpha), float(beta), c_off, ldc,
-                                      nw, wp, C.byref(ev)), "gemm task")
+        if waits:
+            nw, wp = len(waits), (C.c_int * len(waits))(*waits)
+        else:
+            nw, wp = 0, None
+        N.check(self.lib.bx_gemm_task_packed(slot, stream, int(f32), int(ta), int(tb), tri, h, w, n,
+                                             flat.buffer_info()[0], float(alpha), float(beta), c_off,
+                                             ldc, nw, wp,
+                                             C.byref(ev)), "sgemm task" if f32 else "gemm task")
         return ev.value
 
     def trsm(self, slot, stream, right, upper, trans, unit, h, w, alpha, a_off, lda, b_off, ldb,

@@ -27,6 +27,7 @@ class GemmOp(NamedTuple):
     subs: tuple          # ((a_key, b_key, depth), ...)
     k: int
     flops: int
+    keys: frozenset = frozenset()   # the input tiles the launch reads (scratch excluded)
 
 
 class MatOp(NamedTuple):
@@ -82,7 +83,9 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
         if cur is not None:
             subs = tuple(cur[5])
             ops.append(GemmOp(cur[0], cur[1], cur[2], cur[3], cur[4], subs, cur[6],
-                              sum(2 * h * w * d for _, _, d in subs)))
+                              sum(2 * h * w * d for _, _, d in subs),
+                              frozenset(k for ak, bk, _ in subs for k in (ak, bk)
+                                        if k[0] != "#scratch")))
             cur = None
 
     def add(ta, tb, tr, alpha, beta, a, b, d, k):

@@ -691,16 +691,21 @@ class _GpuWorker:
                     res = act.res = self._resolve_op(task, op, res)
                     act.misses_epoch = self._sync_epoch
                 elif opts.l1_enabled:
-                    want = ({k for ak, bk, _ in op.subs for k in (ak, bk) if k[0] != "#scratch"}
-                            if type(op) is GemmOp else {op.key})
-                    want -= res.keys()
+                    want = (op.keys if type(op) is GemmOp else frozenset((op.key,))) - res.keys()
                     if want:
-                        res.update(self._resolve_resident(task, frozenset(want)))
+                        res.update(self._resolve_resident(task, want))
                 if type(op) is GemmOp:
-                    ops_ = [(res[ak], res[bk], d) for ak, bk, d in op.subs]
-                    steps = [(a_[0], a_[1], b_[0], b_[1], d) for a_, b_, d in ops_]
-                    waits = list(dict.fromkeys(
-                        w_ for a_, b_, _ in ops_ for w_ in (a_[2], b_[2]) if w_ is not None))
+                    steps = []
+                    waits = []
+                    for ak, bk, d in op.subs:
+                        a_, b_ = res[ak], res[bk]
+                        steps.append((a_[0], a_[1], b_[0], b_[1], d))
+                        if a_[2] is not None:
+                            waits.append(a_[2])
+                        if b_[2] is not None:
+                            waits.append(b_[2])
+                    if waits:
+                        waits = list(dict.fromkeys(waits))
                     waits += act.pending_waits
                     act.pending_waits = []
                     ev = self._timed(stream, lambda wt, op=op, steps=steps: eng.gemm(

@@ -27,6 +27,8 @@ int bx_gemm_task(int d, int s, int ta, int tb, int tri, int h, int w, int ns, co
 int bx_sgemm_task(int d, int s, int ta, int tb, int h, int w, int ns, const uint64_t *a, const int *la,
                   const uint64_t *b, const int *lb, const int *dp, double al, double be, uint64_t c, int lc,
                   int n, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_gemm_task_packed(int d, int s, int f, int ta, int tb, int tr, int h, int w, int ns, const int64_t *st,
+                        double al, double be, uint64_t c, int lc, int n, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_trsm_tile(int d, int s, int r, int u, int t, int un, int h, int w, double al, uint64_t a, int la,
                  uint64_t b, int lb, int n, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_materialize(int d, int s, int m, int u, int t, int un, int n, uint64_t a, int la, uint64_t o, int lo,
