@@ -87,6 +87,8 @@ class RunOptions:
                                        # stream in (-1 = auto, 0 = off; resident mode only)
     defer_c_move_in: bool = True       # beta*C0 added by a final axpy launch, so a task's
                                        # GEMMs do not wait for its C tile (program.py)
+    critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
+                                       # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
@@ -368,6 +370,12 @@ class _GpuWorker:
                 self.rs.put(stolen)
 
     def _priority(self, task: Task) -> int:
+        w = self.runtime.options.critical_path_weight
+        if w:
+            return self._eq3(task) + w * critical_path(task, self.plan)
+        return self._eq3(task)
+
+    def _eq3(self, task: Task) -> int:
         """Eq. 3: +2 per input-tile reference already in this GPU's L1, +1 per reference
         held by a peer of the same group (counted per step reference, scheduler.py:341-354)."""
         blocks = self.cache._blocks
@@ -821,6 +829,32 @@ class _GpuWorker:
             self._permanent = []
         for blk in self.cache.blocks():
             self._on_evict(blk)
+
+
+def critical_path(task: Task, plan: TaskPlan) -> int:
+    """Length of the longest chain of dependents below ``task`` (0 for a sink; TRSM only
+    has dependency edges, routines.py:426-437).  Computed once per plan, cached on tasks."""
+    cp = getattr(task, "_bx_cp", None)
+    if cp is None:
+        by_id = {t.task_id: t for t in plan.tasks}
+        memo = {}   # explicit post-order DFS over the dependents DAG
+        for root in plan.tasks:
+            if root.task_id in memo:
+                continue
+            stack = [(root, False)]
+            while stack:
+                t, done = stack.pop()
+                if t.task_id in memo:
+                    continue
+                if done:
+                    memo[t.task_id] = max((1 + memo[d] for d in t.dependents), default=0)
+                    continue
+                stack.append((t, True))
+                stack.extend((by_id[d], False) for d in t.dependents if d not in memo)
+        for t in plan.tasks:
+            t._bx_cp = memo[t.task_id]
+        cp = task._bx_cp
+    return cp
 
 
 def task_keys(task: Task) -> dict:

@@ -489,6 +489,11 @@ def _build_runtime_classes():
 
         # ---- Eq. 3 on the shared directory ----
         def _priority(self, task) -> int:
+            w = self.runtime.options.critical_path_weight
+            p = self._eq3(task)
+            return p + w * S.critical_path(task, self.plan) if w else p
+
+        def _eq3(self, task) -> int:
             kx = self._task_index(task)
             blocks = self.cache._blocks
             local = np.fromiter((k in blocks for k in task._bx_klist), dtype=bool, count=len(kx))

@@ -214,3 +214,19 @@ def test_deferred_c_move_in_matches_reference(case, defer):
             assert not has_axpy               # triangle epilogue: C moved in first
         else:
             assert has_axpy and prog.ops[-1] == AxpyOp(res.plan.call.beta)
+
+
+@pytest.mark.parametrize("weight", [1, 100])
+def test_trsm_critical_path_priority(weight):
+    """Eq. 3 plus a critical-path term for the TRSM DAG.  Same numerics; the
+    chain length below a left/lower task (i, j) is (tiles - 1 - i)."""
+    from paper_1510_05041_b200.scheduler import critical_path
+    call = build_call("trsm", m=96, n=64, k=96, tile_size=24, seed=5, uplo="lower",
+                      trsm_scaled=True)
+    x0 = call.c.matrix.as_2d().copy()
+    a = call.a.matrix.as_2d()
+    res = run_call(call, topo(2), RunOptions(critical_path_weight=weight), engine=FakeEngine(2, seed=9))
+    x = call.c.matrix.as_2d()
+    np.testing.assert_allclose(np.tril(a) @ x, x0, rtol=1e-10, atol=1e-10)
+    for t in res.plan.tasks:
+        assert critical_path(t, res.plan) == 4 - 1 - t.out_ref.i
