@@ -515,7 +515,9 @@ def _build_runtime_classes():
                     prow[s] = 0
                     row[s] = t + 1
             while True:
-                live = [(s, int(row[s]) - 1) for s in range(cap) if row[s] != 0]
+                # each slot is read ONCE: a thief may empty it between two reads, and a
+                # second read of 0 would turn into a CAS(0 -> 0) that "claims" task -1
+                live = [(s, v - 1) for s, v in ((s, int(row[s])) for s in range(cap)) if v > 0]
                 if not live:
                     return self._steal()
                 best = None
@@ -539,7 +541,11 @@ def _build_runtime_classes():
                 if n < 2:
                     break
                 row, prow = blk.rs2[v], blk.rsprio2[v]
-                live = [(int(prow[s]), int(row[s]) - 1, s) for s in range(cap) if row[s] != 0]
+                live = []
+                for s in range(cap):
+                    val = int(row[s])            # read once (see _next_entry)
+                    if val > 0:
+                        live.append((int(prow[s]), val - 1, s))
                 if len(live) < 2:
                     continue
                 p, t, s = min(live)

@@ -103,3 +103,32 @@ def check_shared_required(fake):
         return "no error"
     except Exception as exc:
         return type(exc).__name__
+
+
+def run_steal_stress(n, tile, calls, rs_capacity):
+    """Every rank: several calls of one session with small stations (heavy stealing);
+    returns per call (tasks executed by this rank, tasks in the plan, rank 0's max error)."""
+    from paper_1510_05041_b200 import RunOptions, build_call, run_call, spmd
+    from fake_spmd import SpmdFakeEngine
+    sess = spmd.init()
+    call = ref = None
+    if sess.rank == 0:
+        call = build_call("gemm", m=n, n=n, k=n // 2, tile_size=tile, seed=3, alpha=1.0, beta=1.0)
+    call = sess.share_call(call)
+    eng = SpmdFakeEngine(sess.rank, sess.job, seed=sess.rank * 31 + 1)
+    out = []
+    try:
+        for _ in range(calls):
+            if sess.rank == 0:
+                ref = _reference(call)
+            sess.barrier("reference taken")
+            res = run_call(call, options=RunOptions(execution="spmd", rs_capacity=rs_capacity),
+                           engine=eng)
+            err = None
+            if sess.rank == 0:
+                err = float(np.max(np.abs(call.c.matrix.as_2d() - ref)) / max(1.0, np.max(np.abs(ref))))
+            out.append((res.tasks_by_device[sess.rank], len(res.plan.tasks), err))
+            sess.barrier("call checked")
+    finally:
+        eng.cleanup()
+    return out

@@ -86,3 +86,13 @@ def test_spmd_gpu_three_ranks_trsm():
     outs = spmd.launch(3, SC.run_case, "trsm", 2048, 2048, 512, 6, False, timeout=900,
                        devices=[0, 0, 0])
     _check(outs, 3)
+
+
+def test_spmd_station_stealing_stress():
+    """Four ranks with 2-slot stations over three calls: owners pop and thieves steal the
+    same slots concurrently; every task runs exactly once (a slot read twice used to turn a
+    concurrently emptied slot into a claim of task -1, i.e. a duplicate of the last task)."""
+    outs = spmd.launch(6, SC.run_steal_stress, 256, 16, 3, 2, timeout=600)
+    for c in range(3):
+        assert sum(o[c][0] for o in outs) == outs[0][c][1], [o[c] for o in outs]
+        assert outs[0][c][2] <= 1e-11, outs[0][c]
