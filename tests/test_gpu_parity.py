@@ -279,7 +279,10 @@ def test_multi_device_runtime_on_one_gpu(kind, kw, execution):
     a = call.a.matrix.as_2d().copy()
     b = call.b.matrix.as_2d().copy() if call.b is not None else None
     c0 = call.c.matrix.as_2d().copy()
-    res = run_call(call, _virtual_topo(), RunOptions(execution=execution))
+    # small per-device claims (no start-up batch, 1 task per stream, 2-slot stations) so a
+    # per-device thread that starts first cannot drain a 36-task call before the others run
+    res = run_call(call, _virtual_topo(), RunOptions(execution=execution, ramp_tasks=0,
+                                                    tasks_per_stream=1, rs_capacity=2))
     p = dict(kw)
     alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
     ref = c0.copy()
@@ -289,8 +292,27 @@ def test_multi_device_runtime_on_one_gpu(kind, kw, execution):
     m = res.metrics
     assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
     assert m.total_d2d_bytes() == sum(d.d2d_out_bytes for d in m.devices.values())
-    if kind == "gemm":
+    if kind == "gemm" and execution == "deterministic":
+        # one driver thread round-robins the devices: all take tasks and share tiles over L2
         assert m.l2_hits > 0 and len([v for v in res.tasks_by_device.values() if v]) > 1
+
+
+def test_multi_device_concurrent_threads_share_tiles():
+    """One host thread per logical device (execution="concurrent") on a call long enough
+    that every thread joins before the queue drains: tasks spread over the devices and
+    tiles move between them as L2 peer copies."""
+    n, t = 4096, 256
+    call = build_call("gemm", m=n, n=n, k=1024, tile_size=t, seed=23, beta=1.0)
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    res = run_call(call, _virtual_topo(), RunOptions(execution="concurrent", ramp_tasks=0,
+                                                    tasks_per_stream=1, rs_capacity=2))
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=t, alpha=1.0, beta=1.0)
+    assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 1024) <= tolerance.BOUND
+    m = res.metrics
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    assert m.l2_hits > 0 and len([v for v in res.tasks_by_device.values() if v]) > 1
 
 
 def test_multi_device_small_arenas_evict_on_one_gpu():
