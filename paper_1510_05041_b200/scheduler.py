@@ -364,7 +364,7 @@ class _GpuWorker:
             if item is None:
                 break
             self.rs.put(_SlotEntry(self.plan.tasks[item[0]], item[1]))
-        if self.rs.pending_count() == 0:
+        if len(self.runtime.workers) > 1 and self.rs.pending_count() == 0:
             stolen = steal_for(self)
             if stolen is not None:
                 self.rs.put(stolen)
