@@ -806,6 +806,12 @@ def _drive(rt, w, sess) -> None:
 def _child(rank, world, device, job, fn, args, q):
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(device),
                       BX_SPMD_JOB=job)
+    if os.environ.get("BX_SPMD_STACKS"):
+        # debugging aid: `kill -USR1 <pid>` dumps every thread's Python stack to a file
+        import faulthandler
+        import signal
+        faulthandler.register(signal.SIGUSR1, file=open(f"/tmp/bx_stack_{os.getpid()}.txt", "w"),
+                              all_threads=True)
     try:
         out = fn(*args)
         q.put((rank, "ok", out))

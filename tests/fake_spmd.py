@@ -29,8 +29,25 @@ def _shm_array(path, nbytes, create):
 
 
 class SpmdFakeEngine(FakeEngine):
+    """A real GPU keeps executing its streams while the host sleeps; the base fake only
+    advances inside engine calls.  Across processes that matters: a holder that has retired
+    its last task may still have the arrival-flag write behind its final H2D queued, and a
+    peer waits on that flag.  A daemon thread therefore keeps stepping the queues."""
+
     def __init__(self, rank, job, seed=0):
         super().__init__(1, seed=seed)
+        import threading
+        import time
+        self._stop = False
+
+        def progress():
+            while not self._stop:
+                with self._lock:
+                    stepped = self._step()
+                if not stepped:
+                    time.sleep(2e-4)
+        self._progress = threading.Thread(target=progress, daemon=True)
+        self._progress.start()
         self.cuda_ids = [rank]
         self.rank = rank
         self.job = job
@@ -108,6 +125,7 @@ class SpmdFakeEngine(FakeEngine):
             self._enqueue(slot, lane, fn, waits)
 
     def cleanup(self):
+        self._stop = True
         for p in self._files:
             try:
                 os.unlink(p)
