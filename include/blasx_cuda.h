@@ -137,7 +137,7 @@ int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 d
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 256); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);
-/* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16 or 32; default 16) */
+/* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16, 32 or 64; default 16) */
 int bx_set_trsm_rhs(int nr);
 /* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile
  * (default) */

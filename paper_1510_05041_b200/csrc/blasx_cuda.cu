@@ -491,9 +491,13 @@ int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int
     CUDA_TRY(cudaGetLastError());
     return BX_OK;
   }
-  switch (g_trsm_rhs) {
+  // the widest panel not above the knob whose Y block fits in shared memory
+  int nr = g_trsm_rhs;
+  while (nr > 8 && (size_t)t.n * (nr + 4) * sizeof(double) > 200 * 1024) nr /= 2;
+  switch (nr) {
     case 8: { int rc = launch_panel<8>(s, t); if (rc) return rc; break; }
     case 32: { int rc = launch_panel<32>(s, t); if (rc) return rc; break; }
+    case 64: { int rc = launch_panel<64>(s, t); if (rc) return rc; break; }
     default: { int rc = launch_panel<16>(s, t); if (rc) return rc; break; }
   }
   g_launches++;
@@ -1133,7 +1137,8 @@ int bx_set_sgemm_debug(int bits) {
 }
 
 int bx_set_trsm_rhs(int nr) {
-  if (nr != 8 && nr != 16 && nr != 32) return set_err(BX_EINVAL, "trsm panel RHS width must be 8, 16 or 32");
+  if (nr != 8 && nr != 16 && nr != 32 && nr != 64)
+    return set_err(BX_EINVAL, "trsm panel RHS width must be 8, 16, 32 or 64");
   g_trsm_rhs = nr;
   return BX_OK;
 }
