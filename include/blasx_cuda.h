@@ -140,7 +140,7 @@ int bx_set_trsm_leaf(int n);
 /* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16, 32 or 64; default 16) */
 int bx_set_trsm_rhs(int nr);
 /* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile
- * (default) */
+ * (default), 2 = persistent 2-SM with double-buffered TMEM accumulators */
 int bx_set_sgemm_variant(int variant);
 /* tuning knob: load MN-major SGEMM operands with one 3-d TMA box per stage (1, default) or
  * one 2-d box per 32-wide group (0) */

@@ -303,7 +303,10 @@ int tensor_map_f32_mn3d(const float* base, uint64_t rows, uint64_t cols, uint64_
   return BX_OK;
 }
 
-int g_sgemm_variant = 1;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile (default)
+int g_sgemm_variant = 1;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile (default),
+                           // 2: persistent 2-SM with double-buffered TMEM accumulators
+int g_sm_pairs = 74;       // clusters of the persistent SGEMM (one per TPC of a B200)
+int g_sgemm_group = 0;     // persistent SGEMM raster group (m-tiles); 0 = kernel default
 int g_sgemm_mn3d = 1;      // MN-major operands by one 3-d TMA box when the extent allows
 int g_sgemm_debug = 0;     // diagnostic ablation bits (SgemmTask::dbg)
 
@@ -323,6 +326,7 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
     t.mn_lbo = 4096;   // MN-major: 32-wide MN groups (one TMA box) 4 KB apart
     t.mn_sbo = 512;    //           4-row k groups of the 128B_BASE32B atom
     t.dbg = g_sgemm_debug;
+    t.group_m = g_sgemm_group;
     t.a3d = g_sgemm_mn3d && !ta && (h % 32) == 0;
     t.b3d = g_sgemm_mn3d && tb && (w % 32) == 0;
     for (int i = 0; i < n; ++i) {
@@ -333,18 +337,32 @@ int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const fl
       int rc;
       // A: untransposed M x K (MN-major boxes 32x32), transposed K x M (K-major box 32 x 128)
       const CUtensorMapSwizzle MN = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, KM = CU_TENSOR_MAP_SWIZZLE_128B;
-      const uint32_t a_groups = g_sgemm_variant == 1 ? 4u : (uint32_t)(bx::S_BM / 32);
-      const uint32_t b_groups = g_sgemm_variant == 1 ? 4u : (uint32_t)(bx::S_BN / 32);
+      const uint32_t a_groups = g_sgemm_variant >= 1 ? 4u : (uint32_t)(bx::S_BM / 32);
+      const uint32_t b_groups = g_sgemm_variant >= 1 ? 4u : (uint32_t)(bx::S_BN / 32);
       if (!ta && t.a3d) rc = tensor_map_f32_mn3d(a[j], h, d, lda[j], 32, a_groups, &t.steps[i].map_a);
       else if (!ta) rc = tensor_map_f32(a[j], h, d, lda[j], 32, 32, MN, &t.steps[i].map_a);
       else rc = tensor_map_f32(a[j], d, h, lda[j], bx::S_BK, bx::S_BM, KM, &t.steps[i].map_a);
       if (rc) return rc;
       // B: untransposed K x N (K-major box 32 x BN per CTA), transposed N x K (MN boxes 32x32)
-      const uint32_t bn_box = g_sgemm_variant == 1 ? 128u : (uint32_t)bx::S_BN;
+      const uint32_t bn_box = g_sgemm_variant >= 1 ? 128u : (uint32_t)bx::S_BN;
       if (!tb) rc = tensor_map_f32(b[j], d, w, ldb[j], bx::S_BK, bn_box, KM, &t.steps[i].map_b);
       else if (t.b3d) rc = tensor_map_f32_mn3d(b[j], w, d, ldb[j], 32, b_groups, &t.steps[i].map_b);
       else rc = tensor_map_f32(b[j], w, d, ldb[j], 32, 32, MN, &t.steps[i].map_b);
       if (rc) return rc;
+    }
+    if (g_sgemm_variant == 2) {
+      void (*k3)(bx::SgemmTask) = ta ? (tb ? bx::sgemm_tc2p_kernel<1, 1> : bx::sgemm_tc2p_kernel<1, 0>)
+                                     : (tb ? bx::sgemm_tc2p_kernel<0, 1> : bx::sgemm_tc2p_kernel<0, 0>);
+      if (need_attr((const void*)k3)) {
+        CUDA_TRY(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::P_SMEM_BYTES));
+      }
+      const int pair_tiles = ((h + bx::P_BM - 1) / bx::P_BM) * ((w + bx::P_BN - 1) / bx::P_BN);
+      const int clusters = pair_tiles < g_sm_pairs ? pair_tiles : g_sm_pairs;
+      k3<<<2 * clusters, bx::P_THREADS, bx::P_SMEM_BYTES, s>>>(t);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+      if (nsteps <= 0) break;
+      continue;
     }
     if (g_sgemm_variant == 1) {
       void (*k2)(bx::SgemmTask) = ta ? (tb ? bx::sgemm_tc2_kernel<1, 1> : bx::sgemm_tc2_kernel<1, 0>)
@@ -1121,7 +1139,7 @@ int bx_set_gemm_variant(int v) {
 }
 
 int bx_set_sgemm_variant(int v) {
-  if (v < 0 || v > 1) return set_err(BX_EINVAL, "sgemm variant must be 0 or 1");
+  if (v < 0 || v > 2) return set_err(BX_EINVAL, "sgemm variant must be 0, 1 or 2");
   g_sgemm_variant = v;
   return BX_OK;
 }
@@ -1132,7 +1150,9 @@ int bx_set_sgemm_mn3d(int on) {
 }
 
 int bx_set_sgemm_debug(int bits) {
-  g_sgemm_debug = bits;
+  // bits 0..7: ablation switches; bits 8..15: persistent-kernel raster group (tuning)
+  g_sgemm_debug = bits & 0xFF;
+  g_sgemm_group = (bits >> 8) & 0xFF;
   return BX_OK;
 }
 

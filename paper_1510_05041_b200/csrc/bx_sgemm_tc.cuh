@@ -48,6 +48,7 @@ struct SgemmTask {
                        // ring fill, 2 no MMA (results are garbage; timing only)
   int a3d, b3d;        // MN-major operand loaded by ONE 3-d TMA box {32, BK, groups} instead
                        // of one 2-d box per 32-wide group (extent a multiple of 32)
+  int group_m;         // persistent kernel: m-tiles per raster group
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -480,6 +481,207 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   if (warp == 1) {
     s_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(S_TMEM_COLS));
+  }
+}
+
+}  // namespace bx
+
+// ---------------------------------------------------------------------------------------
+// Persistent 2-SM variant (bx_set_sgemm_variant(2)): one 2-CTA cluster per TPC loops over
+// pair tiles (static round robin in the grouped raster order).  TMEM holds two 256-column
+// accumulators, so the MMA thread starts tile t+1 while the epilogue warps drain tile t:
+// the tensor pipe no longer idles through the per-tile epilogue, cluster teardown, CTA
+// launch, TMEM allocation and ring refill of the one-tile-per-cluster kernel.  The stage
+// ring (full/empty) runs on across tiles.  tfull[b] (MMA -> epilogue, multicast commit to
+// both CTAs) and tempty[b] (epilogue -> MMA: the 8 epilogue warps of the pair arrive on
+// the leader's barrier through its cluster address) hand accumulator b back and forth.
+// ---------------------------------------------------------------------------------------
+namespace bx {
+
+__device__ __forceinline__ uint32_t p_leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(s_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void p_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
+template <int TA, int TB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
+    sgemm_tc2p_kernel(const __grid_constant__ SgemmTask t) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)s_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;            // [2] (used in the leader CTA)
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = p_cluster_rank();
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int GROUP_M = t.group_m > 0 ? t.group_m : 4;
+  const int tiles_m = (t.h + P_BM - 1) / P_BM, tiles_n = (t.w + P_BN - 1) / P_BN;
+  const int ntiles = tiles_m * tiles_n;
+  const int per_group = GROUP_M * tiles_n;
+  auto tile_origin = [&](int tile, int& m0, int& n0) {
+    const int first_m = (tile / per_group) * GROUP_M;
+    const int gsize = min(tiles_m - first_m, GROUP_M);
+    m0 = (first_m + (tile % per_group) % gsize) * P_BM;
+    n0 = ((tile % per_group) / gsize) * P_BN;
+  };
+
+  int kslabs = 0;
+  for (int s = 0; s < t.nsteps; ++s) kslabs += (t.steps[s].d + P_BK - 1) / P_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) { s_mbar_init(&full[s], 1); s_mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { s_mbar_init(&tfull[b], 1); s_mbar_init(&tempty[b], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(tmem_slot)), "n"(2 * S_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  s_fence_before();
+  p_cluster_sync();
+  s_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && kslabs > 0) {
+      int it = 0;
+      for (int tile = cluster; tile < ntiles; tile += nclusters) {
+        int m0, n0;
+        tile_origin(tile, m0, n0);
+        const int my_m0 = m0 + 128 * (int)rank, my_n0 = n0 + 128 * (int)rank;
+        int step = 0, k0 = 0, dcur = t.steps[0].d;
+        const CUtensorMap* ma = &t.steps[0].map_a;
+        const CUtensorMap* mb = &t.steps[0].map_b;
+        for (int ks = 0; ks < kslabs; ++ks, ++it) {
+          const int st = it % P_STAGES;
+          if (it >= P_STAGES) p_mbar_wait(&empty[st], ((it / P_STAGES) - 1) & 1);
+          uint8_t* sa = smem + st * P_STAGE_BYTES;
+          uint8_t* sb = sa + P_A_BYTES;
+          if (rank == 0) s_mbar_expect_tx(&full[st], 2 * P_STAGE_BYTES);
+          if (TA) {
+            p_tma_2d_pair(sa, ma, &full[st], k0, my_m0);
+          } else if (t.a3d) {
+            p_tma_3d_pair(sa, ma, &full[st], 0, k0, my_m0 / 32);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p_tma_2d_pair(sa + i * 4096, ma, &full[st], my_m0 + 32 * i, k0);
+          }
+          if (!TB) {
+            p_tma_2d_pair(sb, mb, &full[st], k0, my_n0);
+          } else if (t.b3d) {
+            p_tma_3d_pair(sb, mb, &full[st], 0, k0, my_n0 / 32);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p_tma_2d_pair(sb + i * 4096, mb, &full[st], my_n0 + 32 * i, k0);
+          }
+          k0 += P_BK;
+          if (k0 >= dcur) {
+            k0 = 0;
+            if (++step < t.nsteps) {
+              dcur = t.steps[step].d;
+              ma = &t.steps[step].map_a;
+              mb = &t.steps[step].map_b;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0 && kslabs > 0) {
+      constexpr uint32_t idesc = (s_idesc(!TA, TB) & ~(0x1Fu << 24)) | ((uint32_t)(P_BM >> 4) << 24);
+      const uint32_t sbase = s_u32(smem);
+      const uint64_t da0 = TA ? s_desc(sbase, 16, 1024, 2) : s_desc(sbase, t.mn_lbo, t.mn_sbo, 1);
+      const uint64_t db0 = TB ? s_desc(sbase + P_A_BYTES, t.mn_lbo, t.mn_sbo, 1)
+                              : s_desc(sbase + P_A_BYTES, 16, 1024, 2);
+      constexpr uint32_t AK = TA ? 32 / 16 : 1024 / 16;
+      constexpr uint32_t BKS = TB ? 1024 / 16 : 32 / 16;
+      constexpr uint32_t SU = P_STAGE_BYTES / 16;
+      int it = 0, n = 0;
+      for (int tile = cluster; tile < ntiles; tile += nclusters, ++n) {
+        const int b = n & 1;
+        if (n >= 2) p_mbar_wait(&tempty[b], ((n >> 1) - 1) & 1);   // epilogue drained acc b
+        s_fence_after();
+        const uint32_t acc_tm = tmem + (uint32_t)(b * S_TMEM_COLS);
+        for (int ks = 0; ks < kslabs; ++ks, ++it) {
+          const int st = it % P_STAGES;
+          p_mbar_wait(&full[st], (it / P_STAGES) & 1);
+          s_fence_after();
+          const uint64_t so = (uint64_t)(st * SU);
+#pragma unroll
+          for (int kk = 0; kk < P_BK / 8; ++kk) {
+            const uint32_t acc = (ks + kk) != 0;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                ::"r"(acc_tm), "l"(da0 + so + kk * AK), "l"(db0 + so + kk * BKS), "n"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                       ::"r"(s_u32(&empty[st])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                     ::"r"(s_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t lead_tempty[2] = {p_leader_addr(&tempty[0]), p_leader_addr(&tempty[1])};
+    int n = 0;
+    for (int tile = cluster; tile < ntiles; tile += nclusters, ++n) {
+      const int b = n & 1;
+      int m0, n0;
+      tile_origin(tile, m0, n0);
+      const int row = m0 + 128 * (int)rank + 32 * q + lane;
+      if (kslabs > 0) {
+        p_mbar_wait(&tfull[b], (n >> 1) & 1);
+        s_fence_after();
+      }
+      for (int c0 = 0; c0 < P_BN; c0 += 16) {
+        uint32_t v[16];
+        if (kslabs > 0) {
+          const uint32_t taddr = tmem + (uint32_t)(b * S_TMEM_COLS) + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0u;
+        }
+        if (c0 + 16 >= P_BN && kslabs > 0) {
+          // every TMEM read of accumulator b by this warp is done: hand it back to the MMA
+          s_fence_before();
+          __syncwarp();
+          if (lane == 0) p_arrive_cluster(lead_tempty[b]);
+        }
+        if (row < t.h) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = n0 + c0 + i;
+            if (col < t.w) {
+              float* p = t.c + (size_t)col * t.ldc + row;
+              float r = t.alpha * __uint_as_float(v[i]);
+              if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
+              *p = r;
+            }
+          }
+        }
+      }
+    }
+  }
+  s_fence_before();
+  p_cluster_sync();
+  if (warp == 1) {
+    s_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * S_TMEM_COLS));
   }
 }
 

@@ -209,7 +209,8 @@ def test_concurrent_mode_and_trace():
 
 @pytest.mark.parametrize("variant,mn3d,shape", [(1, 1, (1500, 1300, 1100)), (0, 1, (1500, 1300, 1100)),
                                                 (1, 1, (1536, 1280, 1024)), (0, 1, (1536, 1280, 1024)),
-                                                (1, 0, (1536, 1280, 1024))])
+                                                (1, 0, (1536, 1280, 1024)), (2, 1, (1500, 1300, 1100)),
+                                                (2, 1, (4608, 4352, 1024))])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 def test_sgemm_tcgen05_against_fp64_oracle(ta, tb, variant, mn3d, shape):
     """SGEMM has no reference path (tiling.py:57-60 is float64 only): compare with the
