@@ -341,7 +341,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = p_cluster_rank();
   const int pair = blockIdx.x >> 1;
-  constexpr int GROUP_M = 4;
+  const int GROUP_M = t.group_m > 0 ? t.group_m : 4;
   const int tiles_m = (t.h + P_BM - 1) / P_BM, tiles_n = (t.w + P_BN - 1) / P_BN;
   const int per_group = GROUP_M * tiles_n;
   const int first_m = (pair / per_group) * GROUP_M;
