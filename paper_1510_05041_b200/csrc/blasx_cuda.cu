@@ -38,7 +38,7 @@ int set_err(int code, const std::string& msg) {
                                    std::to_string((int)e_) + ")");                           \
   } while (0)
 
-constexpr int kMaxCompute = 8;
+constexpr int kMaxCompute = 16;
 constexpr int kEvShift = 20;
 
 struct Device {

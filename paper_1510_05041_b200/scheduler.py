@@ -77,7 +77,7 @@ class RunOptions:
     l1_enabled: bool = True
     l2_enabled: bool = True
     record_trace: bool = False
-    n_streams: int = 0                 # compute streams per GPU; 0 = auto (4, TRSM 8)
+    n_streams: int = 0                 # compute streams per GPU; 0 = auto (resolve_streams)
     chunk_steps: int = 16              # k-steps fused per kernel launch
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
     first_chunk_steps: int = 0         # shorter first launch per task; 0 = off
@@ -899,6 +899,21 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
     return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
 
 
+def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOptions:
+    """n_streams=0 (auto): 4 compute streams (the reference's lanes, devices.py:36); TRSM and
+    TRMM 8 (latency-bound diagonal solves / materialisations leave SMs idle unless more
+    tasks overlap); SYRK 12 (its diagonal tasks run half-empty triangle kernels) — but never
+    more in-flight tasks than a quarter of a GPU's share of the plan, so the dynamic
+    schedule keeps tasks to balance at high GPU counts (profiles/streams_sweep_r01.txt)."""
+    if options.n_streams:
+        return options
+    import dataclasses
+    want = {"trsm": 8, "trmm": 8, "syrk": 12}.get(plan.call.kind, 4)
+    share = len(plan.tasks) // max(1, n_devices)
+    cap = max(4, share // (4 * max(1, options.tasks_per_stream)))
+    return dataclasses.replace(options, n_streams=min(want, cap) if want > 4 else want)
+
+
 def resolve_ramp(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOptions:
     """ramp_tasks=-1 (auto): a start-up batch of up to 32 tasks per GPU, but at most a
     quarter of each GPU's share of the plan so the dynamic schedule (stations, stealing,
@@ -916,15 +931,10 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
     from .engine import get_engine
     t_setup0 = time.perf_counter()
     options = options or RunOptions()
-    if not options.n_streams:
-        # 4 streams (the reference's lanes, devices.py:36); TRSM gets 8 because its
-        # diagonal solves are latency-bound and leave SMs idle unless more tasks overlap
-        import dataclasses
-        options = dataclasses.replace(options, n_streams=8 if plan.call.kind == "trsm" else 4)
     if options.execution not in ("deterministic", "concurrent", "spmd"):
         raise ConfigError(f"unknown execution mode {options.execution!r}")
-    if not 1 <= options.n_streams <= 8:
-        raise ConfigError("n_streams must be in 1..8")
+    if not 0 <= options.n_streams <= 16:
+        raise ConfigError("n_streams must be in 1..16")
     if options.chunk_steps < 1:
         raise ConfigError("chunk_steps must be >= 1")
     if options.tasks_per_stream < 1:
@@ -935,6 +945,7 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         return spmd.run_plan_spmd(plan, options, engine, _t_plan=_t_plan)
     topology = topology or discover_topology()
     devs = topology.accelerators()
+    options = resolve_streams(plan, options, len(devs))
     options = resolve_ramp(plan, options, len(devs))
     if engine is None:
         engine = get_engine([d.device_id for d in devs], options.n_streams,

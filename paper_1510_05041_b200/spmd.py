@@ -640,6 +640,7 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
     SpmdRuntime, SpmdWorker = _classes()
     t_setup0 = time.perf_counter()
     r, W = sess.rank, sess.world
+    options = S.resolve_streams(plan, options, W)
     options = S.resolve_ramp(plan, options, W)
     if options.rs_capacity > RS_SLOTS:
         raise ConfigError(f"spmd execution supports rs_capacity <= {RS_SLOTS}")
