@@ -325,3 +325,35 @@ def test_multi_device_small_arenas_evict_on_one_gpu():
     ref = c0.copy()
     tiled.run_tiled("gemm", a, ref, b, tile_size=256, alpha=1.0, beta=1.0)
     assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 2048) <= 10
+
+
+def _random_cases(n_cases=40, seed=2026):
+    import routine_cases as G
+    return G.random_cases(n_cases, seed)
+
+
+@pytest.mark.parametrize("case", _random_cases(), ids=lambda c: f"r{c[0]}_{c[1]}")
+def test_randomized_routines_against_oracle(case):
+    """Seeded random shapes (ragged, 1..639), tile sizes, flags, scalars and runtime options
+    for every routine, against the tiled oracle with the north-star bound (and the TRSM
+    residual bound) — the GPU counterpart of the reference's randomized acceptance sweep
+    (tests/test_acceptance.py:595-619)."""
+    _, kind, m, n, k, t, kw, opts = case
+    call = build_call(kind, m=m, n=n, k=k, tile_size=t, seed=m * 7 + n, trsm_scaled=True, **kw)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    res = run_call(call, options=RunOptions(**opts))
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    out = call.c.matrix.as_2d()
+    p = dict(kw)
+    alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
+    ref = c0.copy()
+    tiled.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
+    side = p.get("side", "left")
+    kk = k if kind in ("gemm", "syrk", "syr2k") else (m if side == "left" else n)
+    assert _ratio(kind, out, ref, a, b, c0, alpha, beta, kk) <= tolerance.BOUND
+    if kind == "trsm":
+        tri, _ = tiled.tri_of(a, p.get("uplo", "upper"), p.get("diag", "non-unit"),
+                              p.get("trans_a", False))
+        assert tolerance.trsm_residual_ratio(tri, out, c0, alpha, side, EPS) <= tolerance.BOUND

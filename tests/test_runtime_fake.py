@@ -230,3 +230,29 @@ def test_trsm_critical_path_priority(weight):
     np.testing.assert_allclose(np.tril(a) @ x, x0, rtol=1e-10, atol=1e-10)
     for t in res.plan.tasks:
         assert critical_path(t, res.plan) == 4 - 1 - t.out_ref.i
+
+
+def _fake_random_cases():
+    import routine_cases as G
+    return G.random_cases(24, seed=77)
+
+
+@pytest.mark.parametrize("case", _fake_random_cases(), ids=lambda c: f"r{c[0]}_{c[1]}")
+def test_randomized_routines_fake_engine(case):
+    """The GPU randomized sweep's case generator on the fake engine (2 devices, randomised
+    stream interleaving): runtime options x routines x ragged shapes vs the oracle."""
+    from oracle import tiled as OT
+    from oracle import tolerance as TOL
+    _, kind, m, n, k, t, kw, opts = case
+    call = build_call(kind, m=m, n=n, k=k, tile_size=t, seed=m * 7 + n, trsm_scaled=True, **kw)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    res = run_call(call, topo(2, arena=64 << 20), RunOptions(**opts), engine=FakeEngine(2, seed=m))
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    p = dict(kw)
+    alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
+    ref = c0.copy()
+    OT.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-10,
+                               atol=1e-10 * max(1.0, float(np.max(np.abs(ref)))))
