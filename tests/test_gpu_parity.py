@@ -327,7 +327,7 @@ def test_multi_device_small_arenas_evict_on_one_gpu():
     assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 2048) <= 10
 
 
-def _random_cases(n_cases=40, seed=2026):
+def _random_cases(n_cases=120, seed=2026):
     import routine_cases as G
     return G.random_cases(n_cases, seed)
 
@@ -357,3 +357,29 @@ def test_randomized_routines_against_oracle(case):
         tri, _ = tiled.tri_of(a, p.get("uplo", "upper"), p.get("diag", "non-unit"),
                               p.get("trans_a", False))
         assert tolerance.trsm_residual_ratio(tri, out, c0, alpha, side, EPS) <= tolerance.BOUND
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_randomized_sgemm_against_fp64_oracle(i):
+    """Random ragged SGEMM calls (tcgen05 kind::tf32) vs the float64 oracle.  The MMA rounds
+    its inputs to TF32 (10-bit mantissa): relative to a bound with the fp32 epsilon
+    (2^-23) the error ratio falls like k^-1.5, so the fp32-epsilon bound holds from k ~ 200
+    (and at every BASELINE shape) while small k is held to the TF32 unit roundoff 2^-11."""
+    rng = np.random.default_rng(500 + i)
+    m, n, k = (int(x) for x in rng.integers(1, 900, size=3))
+    ta, tb = bool(rng.integers(2)), bool(rng.integers(2))
+    t = int(rng.choice([128, 256, 512]))
+    alpha, beta = float(rng.choice([1.0, -0.5])), float(rng.choice([0.0, 1.0]))
+    call = build_call("gemm", m=m, n=n, k=k, tile_size=t, seed=i, alpha=alpha, beta=beta,
+                      trans_a=ta, trans_b=tb, dtype=np.float32)
+    a = call.a.matrix.as_2d().astype(np.float64)
+    b = call.b.matrix.as_2d().astype(np.float64)
+    c0 = call.c.matrix.as_2d().astype(np.float64)
+    run_call(call, options=RunOptions(chunk_steps=int(rng.choice([1, 16]))))
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=t, alpha=alpha, beta=beta, trans_a=ta, trans_b=tb)
+    eps = float(np.finfo(np.float32).eps) if k >= 256 else 2.0 ** -11
+    r = tolerance.gemm_ratio(call.c.matrix.as_2d().astype(np.float64), ref, a_norm=np.linalg.norm(a),
+                             b_norm=np.linalg.norm(b), k=k, alpha=alpha, beta=beta,
+                             c0_norm=np.linalg.norm(c0), eps=eps)
+    assert r <= tolerance.BOUND, (r, k)
