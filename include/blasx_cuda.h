@@ -132,8 +132,10 @@ int bx_dev_copy_h2d(int dev, uint64_t dst, const void* src, uint64_t bytes);
 int bx_dev_copy_d2h(int dev, void* dst, uint64_t src, uint64_t bytes);
 int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, double alpha,
                     uint64_t a, int lda, uint64_t b, int ldb, double beta, uint64_t c, int ldc);
-/* tuning knob: tile configuration of the FP64 task GEMM (0 default; 1, 2 alternates) */
-int bx_set_gemm_variant(int variant);  /* 0 mbarrier ring (default), 1 wide, 2 deep, 3 slack-2 */
+/* tuning knob: tile configuration of the FP64 task GEMM: 0 (default) mbarrier ring, 16 warps
+ * of 32x32; 9 the same ring with 8 warps of 64x32; 1 wide, 2 deep (__syncthreads rings);
+ * 3 slack-2, 5 two CTAs/SM, 6 BK 32, 7 no slack; 8 TMA-fed */
+int bx_set_gemm_variant(int variant);
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 256); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);

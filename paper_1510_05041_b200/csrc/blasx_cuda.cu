@@ -191,12 +191,12 @@ int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
     case 1: return launch_gemm_cfg<bx::CfgWide, TA, TB>(t, s);
     case 2: return launch_gemm_cfg<bx::CfgDeep, TA, TB>(t, s);
     case 3: return launch_gemm_ws<bx::CfgMb2, TA, TB>(t, s);
-    case 4: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s);
     case 5: return launch_gemm_ws<bx::CfgMbPair, TA, TB>(t, s);
     case 6: return launch_gemm_ws<bx::CfgMbK32, TA, TB>(t, s);
     case 7: return launch_gemm_ws<bx::CfgMbS0, TA, TB>(t, s);
+    case 9: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s);      // 8 warps of 64x32
     case 99: return launch_gemm_ws<bx::CfgMbNoLoad, TA, TB>(t, s);
-    default: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s);
+    default: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s);   // 16 warps of 32x32
   }
 }
 
