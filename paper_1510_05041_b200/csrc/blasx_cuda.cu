@@ -195,6 +195,10 @@ int launch_gemm_t(const bx::GemmTask& t, cudaStream_t s) {
     case 6: return launch_gemm_ws<bx::CfgMbK32, TA, TB>(t, s);
     case 7: return launch_gemm_ws<bx::CfgMbS0, TA, TB>(t, s);
     case 9: return launch_gemm_ws<bx::CfgMb, TA, TB>(t, s);      // 8 warps of 64x32
+    case 10: return launch_gemm_ws<bx::CfgMb16S0, TA, TB>(t, s);
+    case 11: return launch_gemm_ws<bx::CfgMb16S2, TA, TB>(t, s);
+    case 12: return launch_gemm_ws<bx::CfgMb16K32, TA, TB>(t, s);
+    case 13: return launch_gemm_ws<bx::CfgMb16x64, TA, TB>(t, s);
     case 99: return launch_gemm_ws<bx::CfgMbNoLoad, TA, TB>(t, s);
     default: return launch_gemm_ws<bx::CfgMb16, TA, TB>(t, s);   // 16 warps of 32x32
   }

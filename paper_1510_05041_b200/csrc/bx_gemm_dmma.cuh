@@ -243,6 +243,10 @@ using CfgMbPair = MbCfg<64, 128, 16, 32, 64, 3, 0, 2>;
 using CfgMbK32 = MbCfg<128, 128, 32, 64, 32, 3, 0>;    // BK 32, 3 stages (221 KB)
 using CfgMbS0 = MbCfg<128, 128, 16, 64, 32, 5, 0>;     // no slack, prefetch distance 4
 using CfgMbNoLoad = MbCfg<128, 128, 16, 64, 32, 5, 1, 1, true>;   // experiment only
+using CfgMb16S0 = MbCfg<128, 128, 16, 32, 32, 5, 0>;   // 16 warps, no slack
+using CfgMb16S2 = MbCfg<128, 128, 16, 32, 32, 5, 2>;   // 16 warps, slack 2
+using CfgMb16K32 = MbCfg<128, 128, 32, 32, 32, 3, 0>;  // 16 warps, BK 32, 3 stages
+using CfgMb16x64 = MbCfg<128, 128, 16, 32, 64, 5, 1>;  // 8 warps of 32x64
 using CfgMbPairS = MbCfg<64, 128, 16, 32, 64, 3, 1, 2>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
