@@ -78,7 +78,8 @@ class RunOptions:
     l2_enabled: bool = True
     record_trace: bool = False
     n_streams: int = 0                 # compute streams per GPU; 0 = auto (resolve_streams)
-    chunk_steps: int = 16              # k-steps fused per kernel launch
+    chunk_steps: int = 0               # k-steps fused per kernel launch; 0 = auto
+                                       # (resolve_streams: GEMM/SYMM 8, others 16)
     tasks_per_stream: int = 2          # tasks kept issued per compute stream (lookahead)
     first_chunk_steps: int = 0         # shorter first launch per task; 0 = off
     ramp_tasks: int = -1               # start-up batch: the first N tasks a GPU starts run
@@ -900,15 +901,22 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
 
 
 def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOptions:
-    """n_streams=0 (auto): 4 compute streams (the reference's lanes, devices.py:36); TRSM and
-    TRMM 8 (latency-bound diagonal solves / materialisations leave SMs idle unless more
-    tasks overlap); SYRK 12 (its diagonal tasks run half-empty triangle kernels) — but never
-    more in-flight tasks than a quarter of a GPU's share of the plan, so the dynamic
-    schedule keeps tasks to balance at high GPU counts (profiles/streams_sweep_r01.txt)."""
+    """Auto launch shape.  chunk_steps=0: 8 k-steps per launch for GEMM/SYMM, 16 otherwise.
+    n_streams=0: 4 compute streams (the reference's lanes, devices.py:36); GEMM/SYMM, TRSM
+    and TRMM 8 (more independent launches in flight; latency-bound diagonal solves /
+    materialisations leave SMs idle otherwise); SYRK 12 (its diagonal tasks run half-empty
+    triangle kernels) — but never more in-flight tasks than a quarter of a GPU's share of
+    the plan, so the dynamic schedule keeps tasks to balance at high GPU counts
+    (profiles/streams_sweep_r01.txt, profiles/chunk_streams_sweep_r01.txt)."""
+    import dataclasses
+    kind = plan.call.kind
+    if not options.chunk_steps:
+        # GEMM-only tasks: 8-step launches interleave better across the streams than one
+        # 16-step launch per task (cfg2 255.8 -> 252.4 ms with 8 streams)
+        options = dataclasses.replace(options, chunk_steps=8 if kind in ("gemm", "symm") else 16)
     if options.n_streams:
         return options
-    import dataclasses
-    want = {"trsm": 8, "trmm": 8, "syrk": 12}.get(plan.call.kind, 4)
+    want = {"trsm": 8, "trmm": 8, "syrk": 12, "gemm": 8, "symm": 8}.get(kind, 4)
     share = len(plan.tasks) // max(1, n_devices)
     cap = max(4, share // (4 * max(1, options.tasks_per_stream)))
     return dataclasses.replace(options, n_streams=min(want, cap) if want > 4 else want)
@@ -935,8 +943,8 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
         raise ConfigError(f"unknown execution mode {options.execution!r}")
     if not 0 <= options.n_streams <= 16:
         raise ConfigError("n_streams must be in 1..16")
-    if options.chunk_steps < 1:
-        raise ConfigError("chunk_steps must be >= 1")
+    if options.chunk_steps < 0:
+        raise ConfigError("chunk_steps must be >= 1 (0 = auto)")
     if options.tasks_per_stream < 1:
         raise ConfigError("tasks_per_stream must be >= 1")
     if options.execution == "spmd":
