@@ -147,8 +147,9 @@ int bx_set_sgemm_variant(int variant);
 /* tuning knob: load MN-major SGEMM operands with one 3-d TMA box per stage (1, default) or
  * one 2-d box per 32-wide group (0) */
 int bx_set_sgemm_mn3d(int on);
-/* diagnostic: SGEMM ablation bits (1 = skip TMA loads after the first ring fill, 2 = skip
- * the MMAs); results are garbage while set — timing experiments only, default 0 */
+/* diagnostic: SGEMM ablation bits 0-7 (1 = skip TMA loads after the first ring fill, 2 =
+ * skip the MMAs, 8 = skip the C stores; results are garbage while set — timing experiments
+ * only) and, in bits 8-15, the raster group (m-tiles) of the 2-SM kernels (0 = default 4) */
 int bx_set_sgemm_debug(int bits);
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha,
                     uint64_t a, int lda, uint64_t b, int ldb, float beta, uint64_t c, int ldc);
