@@ -147,6 +147,9 @@ int bx_set_sgemm_variant(int variant);
 /* tuning knob: load MN-major SGEMM operands with one 3-d TMA box per stage (1, default) or
  * one 2-d box per 32-wide group (0) */
 int bx_set_sgemm_mn3d(int on);
+/* SGEMM accuracy mode: 0 (default) TF32 inputs; 1 = 3xTF32 (hi*hi + hi*lo + lo*hi of a
+ * TF32 hi/lo split of each operand): ~fp32 accuracy at a third of the tensor rate */
+int bx_set_sgemm_precise(int on);
 /* diagnostic: SGEMM ablation bits 0-7 (1 = skip TMA loads after the first ring fill, 2 =
  * skip the MMAs, 8 = skip the C stores; results are garbage while set — timing experiments
  * only) and, in bits 8-15, the raster group (m-tiles) of the 2-SM kernels (0 = default 4) */

@@ -315,10 +315,56 @@ int g_sgemm_mn3d = 1;      // MN-major operands by one 3-d TMA box when the exte
 int g_sgemm_debug = 0;     // diagnostic ablation bits (SgemmTask::dbg)
 
 // fp32 task GEMM on tcgen05 (TF32 inputs, fp32 accumulation in TMEM)
+int g_sgemm_precise = 0;   // 1: 3xTF32 split products (~fp32 accuracy, a third of the rate)
+
+int sgemm_tf32(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
+               const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c, int ldc);
+
+// precise mode: per step, split op(A_s) and op(B_s) storage into TF32 hi/lo copies (stream-
+// ordered scratch) and accumulate hi*hi + hi*lo + lo*hi with the TF32 kernels
+int sgemm_precise(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
+                  const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c,
+                  int ldc) {
+  for (int i = 0; i < nsteps; ++i) {
+    const int d = depth[i];
+    const int ar = ta ? d : h, ac = ta ? h : d;       // stored extents of A_s
+    const int br = tb ? w : d, bc = tb ? d : w;       // stored extents of B_s
+    const int lda4 = (ar + 3) & ~3, ldb4 = (br + 3) & ~3;
+    const size_t abytes = (size_t)lda4 * ac * 4, bbytes = (size_t)ldb4 * bc * 4;
+    void* buf = nullptr;
+    CUDA_TRY(cudaMallocAsync(&buf, 2 * abytes + 2 * bbytes + 64, s));
+    float* ahi = (float*)buf;
+    float* alo = (float*)((char*)buf + abytes);
+    float* bhi = (float*)((char*)buf + 2 * abytes);
+    float* blo = (float*)((char*)buf + 2 * abytes + bbytes);
+    dim3 blk(32, 8);
+    bx::tf32_split_kernel<<<dim3((ar + 31) / 32, (ac + 7) / 8), blk, 0, s>>>(a[i], lda[i], ar, ac, ahi, alo, lda4);
+    bx::tf32_split_kernel<<<dim3((br + 31) / 32, (bc + 7) / 8), blk, 0, s>>>(b[i], ldb[i], br, bc, bhi, blo, ldb4);
+    g_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    const float* ap[3] = {ahi, ahi, alo};
+    const float* bp[3] = {bhi, blo, bhi};
+    int la[3] = {lda4, lda4, lda4}, lb[3] = {ldb4, ldb4, ldb4}, dd[3] = {d, d, d};
+    // one 3-step launch: hi*hi + hi*lo + lo*hi (C read once, beta only on the first step)
+    int rc = sgemm_tf32(s, ta, tb, h, w, 3, ap, la, bp, lb, dd, alpha, i == 0 ? beta : 1.0f, c, ldc);
+    CUDA_TRY(cudaFreeAsync(buf, s));
+    if (rc) return rc;
+  }
+  return BX_OK;
+}
+
 int sgemm_raw(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
               const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c, int ldc) {
   if (h <= 0 || w <= 0) return BX_OK;
   if (ldc < h) return set_err(BX_EINVAL, "sgemm: ldc < h");
+  if (g_sgemm_precise && nsteps > 0)
+    return sgemm_precise(s, ta, tb, h, w, nsteps, a, lda, b, ldb, depth, alpha, beta, c, ldc);
+  return sgemm_tf32(s, ta, tb, h, w, nsteps, a, lda, b, ldb, depth, alpha, beta, c, ldc);
+}
+
+// fp32 task GEMM on tcgen05.mma.kind::tf32 (the kernels above)
+int sgemm_tf32(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const float* const* a, const int* lda,
+               const float* const* b, const int* ldb, const int* depth, float alpha, float beta, float* c, int ldc) {
   for (int s0 = 0; s0 < (nsteps > 0 ? nsteps : 1); s0 += bx::S_MAX_STEPS) {
     bx::SgemmTask t;
     memset(&t, 0, sizeof(t));
@@ -1145,6 +1191,11 @@ int bx_set_gemm_variant(int v) {
 int bx_set_sgemm_variant(int v) {
   if (v < 0 || v > 2) return set_err(BX_EINVAL, "sgemm variant must be 0, 1 or 2");
   g_sgemm_variant = v;
+  return BX_OK;
+}
+
+int bx_set_sgemm_precise(int on) {
+  g_sgemm_precise = on != 0;
   return BX_OK;
 }
 

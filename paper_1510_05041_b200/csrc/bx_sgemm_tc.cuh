@@ -686,3 +686,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 }
 
 }  // namespace bx
+
+// ---------------------------------------------------------------------------------------
+// 3xTF32 split for the precise SGEMM mode (bx_set_sgemm_precise): x = hi + lo with hi the
+// TF32-rounded value (low 13 mantissa bits zero, so the tensor core takes it exactly) and
+// lo = x - hi (exact in fp32).  A*B ~= hi_a*hi_b + hi_a*lo_b + lo_a*hi_b restores ~fp32
+// accuracy at a third of the TF32 rate.  Strided rows x cols column-major input -> two
+// packed (ld = rows rounded up to 4) outputs.
+// ---------------------------------------------------------------------------------------
+namespace bx {
+
+__global__ void tf32_split_kernel(const float* __restrict__ x, int ldx, int rows, int cols, float* __restrict__ hi,
+                                  float* __restrict__ lo, int ldo) {
+  const int r = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.y * 8 + threadIdx.y;
+  if (r >= rows || c >= cols) return;
+  const float v = x[(size_t)c * ldx + r];
+  uint32_t u = __float_as_uint(v);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;   // round to 10-bit mantissa
+  const float h = __uint_as_float(u);
+  hi[(size_t)c * ldo + r] = h;
+  lo[(size_t)c * ldo + r] = v - h;
+}
+
+}  // namespace bx
+

@@ -383,3 +383,31 @@ def test_randomized_sgemm_against_fp64_oracle(i):
                              b_norm=np.linalg.norm(b), k=k, alpha=alpha, beta=beta,
                              c0_norm=np.linalg.norm(c0), eps=eps)
     assert r <= tolerance.BOUND, (r, k)
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_sgemm_precise_mode_meets_fp32_bound_at_small_k(i):
+    """3xTF32 mode (bx_set_sgemm_precise): the hi/lo split products restore the north-star
+    bound with the fp32 epsilon even at small k, where plain TF32 exceeds it."""
+    from paper_1510_05041_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(900 + i)
+    m, n, k = int(rng.integers(100, 900)), int(rng.integers(100, 900)), int(rng.integers(8, 120))
+    ta, tb = bool(rng.integers(2)), bool(rng.integers(2))
+    call = build_call("gemm", m=m, n=n, k=k, tile_size=256, seed=i, alpha=1.0, beta=1.0,
+                      trans_a=ta, trans_b=tb, dtype=np.float32)
+    a = call.a.matrix.as_2d().astype(np.float64)
+    b = call.b.matrix.as_2d().astype(np.float64)
+    c0 = call.c.matrix.as_2d().astype(np.float64)
+    lib.bx_set_sgemm_precise(1)
+    try:
+        run_call(call)
+    finally:
+        lib.bx_set_sgemm_precise(0)
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=256, alpha=1.0, beta=1.0, trans_a=ta, trans_b=tb)
+    r = tolerance.gemm_ratio(call.c.matrix.as_2d().astype(np.float64), ref, a_norm=np.linalg.norm(a),
+                             b_norm=np.linalg.norm(b), k=k, alpha=1.0, beta=1.0,
+                             c0_norm=np.linalg.norm(c0), eps=float(np.finfo(np.float32).eps))
+    assert r <= tolerance.BOUND, (r, m, n, k)
+
