@@ -88,6 +88,8 @@ class RunOptions:
                                        # stream in (-1 = auto, 0 = off; resident mode only)
     defer_c_move_in: bool = True       # beta*C0 added by a final axpy launch, so a task's
                                        # GEMMs do not wait for its C tile (program.py)
+    sgemm_precise: bool = False        # float32 calls: 3xTF32 (fp32 accuracy, 1/3 rate)
+                                       # instead of TF32 inputs (process-wide engine knob)
     critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
                                        # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
@@ -978,6 +980,8 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
                 f"{WORKING_SET_TILES}-tile working set at tile size {plan.tile_size}")
         caps[slot] = want
     engine.ensure_arenas(caps)
+    if plan.dtype.itemsize == 4 and hasattr(engine, "lib"):
+        engine.lib.bx_set_sgemm_precise(int(options.sgemm_precise))
     if plan.snapshot_alias is not None:
         snap = plan.matrices[plan.snapshot_alias]
         snap_bytes = (-(-snap.rows // plan.tile_size) * device_ld(plan.tile_size)

@@ -664,6 +664,8 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
                 f"rank {r}: the call's working set ({full} bytes) does not fit in HBM; spmd "
                 f"execution keeps every tile resident")
         engine.ensure_arenas({slot: want})
+    if plan.dtype.itemsize == 4 and hasattr(engine, "lib"):
+        engine.lib.bx_set_sgemm_precise(int(options.sgemm_precise))
     sess.publish_arena(engine, slot)
     pinned_here = [m.storage for m in plan.matrices.values() if engine.register_host(m.storage)]
 

@@ -399,9 +399,8 @@ def test_sgemm_precise_mode_meets_fp32_bound_at_small_k(i):
     a = call.a.matrix.as_2d().astype(np.float64)
     b = call.b.matrix.as_2d().astype(np.float64)
     c0 = call.c.matrix.as_2d().astype(np.float64)
-    lib.bx_set_sgemm_precise(1)
     try:
-        run_call(call)
+        run_call(call, options=RunOptions(sgemm_precise=True))
     finally:
         lib.bx_set_sgemm_precise(0)
     ref = c0.copy()
