@@ -136,6 +136,9 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
  * of 32x32; 9 the same ring with 8 warps of 64x32; 1 wide, 2 deep (__syncthreads rings);
  * 3 slack-2, 5 two CTAs/SM, 6 BK 32, 7 no slack; 8 TMA-fed */
 int bx_set_gemm_variant(int variant);
+/* tuning knob: raster group (consecutive m-tiles per grid column group) of the FP64 task
+ * GEMM, default 8 */
+int bx_set_gemm_group(int group);
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 256); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);

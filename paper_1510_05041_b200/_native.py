@@ -79,6 +79,7 @@ _SIGS = {
     "bx_set_sgemm_debug": [_i],
     "bx_set_sgemm_mn3d": [_i],
     "bx_set_sgemm_precise": [_i],
+    "bx_set_gemm_group": [_i],
     "bx_set_sgemm_variant": [_i],
     "bx_last_error": [C.c_char_p, _i],
     "bx_ipc_arena_handle": [_i, _p, _pu64],
@@ -119,7 +120,8 @@ def load(path: str = _LIB_PATH):
         for env, fn in (("BX_GEMM_VARIANT", "bx_set_gemm_variant"),
                         ("BX_SGEMM_VARIANT", "bx_set_sgemm_variant"),
                         ("BX_TRSM_LEAF", "bx_set_trsm_leaf"), ("BX_TRSM_RHS", "bx_set_trsm_rhs"),
-                        ("BX_SGEMM_PRECISE", "bx_set_sgemm_precise")):
+                        ("BX_SGEMM_PRECISE", "bx_set_sgemm_precise"),
+                        ("BX_GEMM_GROUP", "bx_set_gemm_group")):
             if os.environ.get(env):
                 getattr(lib, fn)(int(os.environ[env]))
         _lib = lib

@@ -156,6 +156,7 @@ bool need_attr(const void* kernel) {
 }
 
 int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
+int g_gemm_group = 8;    // raster group (m-tiles) of the FP64 task GEMM grid
 int g_trsm_rhs = 16;     // right-hand sides per CTA of the TRSM panel kernel (8/16/32)
 int g_trsm_leaf = 256;   // triangle order solved by a leaf kernel; larger ones recurse
 
@@ -452,7 +453,7 @@ int gemm_tma(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
   for (int s0 = 0; s0 < nsteps; s0 += bx::T_MAX_STEPS) {
     bx::GemmTmaTask t;
     memset(&t, 0, sizeof(t));
-    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = 8;
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = g_gemm_group;
     t.alpha = alpha;
     t.beta = (s0 == 0) ? beta : 1.0;
     const int n = nsteps - s0 < bx::T_MAX_STEPS ? nsteps - s0 : bx::T_MAX_STEPS;
@@ -496,14 +497,14 @@ int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
   if (nsteps == 0) {
     // C = beta*C (beta==0 -> zero) — expressed as a zero-depth task
     bx::GemmTask t{};
-    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.nsteps = 0; t.tri = tri; t.group_m = 8;
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.nsteps = 0; t.tri = tri; t.group_m = g_gemm_group;
     t.alpha = alpha; t.beta = beta;
     return launch_gemm(ta, tb, t, s);
   }
   if (g_gemm_variant == 8) return gemm_tma(s, ta, tb, tri, h, w, nsteps, a, lda, b, ldb, depth, alpha, beta, c, ldc);
   for (int s0 = 0; s0 < nsteps; s0 += bx::G_MAX_STEPS) {
     bx::GemmTask t{};
-    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = 8;
+    t.c = c; t.ldc = ldc; t.h = h; t.w = w; t.tri = tri; t.group_m = g_gemm_group;
     t.alpha = alpha;
     t.beta = (s0 == 0) ? beta : 1.0;
     int n = nsteps - s0 < bx::G_MAX_STEPS ? nsteps - s0 : bx::G_MAX_STEPS;
@@ -1181,6 +1182,12 @@ int bx_dgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, do
   const double* ap = (const double*)a;
   const double* bp = (const double*)b;
   return gemm_raw(s, ta, tb, 0, m, n, 1, &ap, &lda, &bp, &ldb, &k, alpha, beta, (double*)c, ldc);
+}
+
+int bx_set_gemm_group(int g) {
+  if (g < 1 || g > 64) return set_err(BX_EINVAL, "gemm raster group must be in [1, 64]");
+  g_gemm_group = g;
+  return BX_OK;
 }
 
 int bx_set_gemm_variant(int v) {

@@ -58,6 +58,7 @@ int bx_set_trsm_rhs() { return 0; }
 int bx_set_sgemm_debug() { return 0; }
 int bx_set_sgemm_mn3d() { return 0; }
 int bx_set_sgemm_precise() { return 0; }
+int bx_set_gemm_group() { return 0; }
 int bx_set_sgemm_variant() { return 0; }
 int bx_sgemm_device() { return 0; }
 int bx_fp64_peak_probe(int d, int it, double *tf) { *tf = 37.0; return 0; }
