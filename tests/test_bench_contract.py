@@ -1,0 +1,61 @@
+"""bench.py's JSON line (the driver's contract) assembled from synthetic leg results on CPU,
+and the runtime's automatic launch-shape resolution."""
+
+import json
+import os
+import sys
+import types
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_1510_05041_b200 import RunOptions, build_call  # noqa: E402
+from paper_1510_05041_b200.routines import generate_tasks  # noqa: E402
+from paper_1510_05041_b200.scheduler import resolve_ramp, resolve_streams  # noqa: E402
+
+REQUIRED = ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+            "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "clocks",
+            "roofline"]
+
+
+class _Clk:
+    def summary(self):
+        return {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": [], "samples": 3}
+
+
+def test_result_line_has_the_contract_keys():
+    args = types.SimpleNamespace(gpus=1, steps=3, warmup=3, chunk=0)
+    cfg = bench.CONFIGS["cfg2"]
+    val = dict(value=35.7, ms_per_step=246.0, launches=3, kernel_tflops=35.7, avg_launch_ms=246.0,
+               flops_per_launch=8.8e12)
+    e2e = dict(value=34.8, ms=252.0, flops=8.8e12, launches=1536, sweep=[], h2d=6.44e9, d2h=2.15e9,
+               p2p=0, l1=7680, l2=0, host=512, per_device={"0": dict(h2d=6.44e9, d2d_in=0, tasks=256)})
+    cpu = dict(value=0.45, unit="TFLOP/s", cores=16, kind="port", sample="x", seconds=10.0)
+    line = bench.result_line(args, cfg, val, e2e, 37.1, _Clk(), cpu, False)
+    json.dumps(line)
+    assert [k for k in REQUIRED if k not in line] == []
+    assert line["e2e"]["h2d_bytes_per_step"] == 6.44e9 and line["e2e"]["unit"] == "TFLOP/s"
+    r = line["roofline"]
+    assert r["bound"] == "tensor" and r["frac"] == pytest.approx(35.7 / 37.1)
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 16
+    assert line["higher_is_better"] is True and line["vs_baseline"] is None
+
+
+@pytest.mark.parametrize("kind,k,ndev,chunk,streams", [
+    ("gemm", 1024, 1, 8, 8), ("gemm", 1024, 8, 8, 4), ("symm", 1024, 1, 8, 8),
+    ("syrk", 512, 1, 16, 12), ("syrk", 512, 8, 16, 4), ("trsm", 1024, 1, 16, 8),
+    ("trmm", 1024, 1, 16, 8), ("syr2k", 512, 1, 16, 4)])
+def test_auto_launch_shape(kind, k, ndev, chunk, streams):
+    # the BASELINE task grids (16 x 16 tiles; K = 16 or 8 steps) at a small element count
+    call = build_call(kind, m=1024, n=1024, k=k, tile_size=64, seed=0, uplo="lower",
+                      beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0)
+    plan = generate_tasks(call)
+    o = resolve_ramp(plan, resolve_streams(plan, RunOptions(), ndev), ndev)
+    assert (o.chunk_steps, o.n_streams) == (chunk, streams)
+    assert 0 <= o.ramp_tasks <= max(0, len(plan.tasks) // (4 * ndev))
+    # explicit values are kept
+    o2 = resolve_streams(plan, RunOptions(chunk_steps=3, n_streams=2), ndev)
+    assert (o2.chunk_steps, o2.n_streams) == (3, 2)
