@@ -142,7 +142,7 @@ int bx_set_gemm_group(int group);
 /* tuning knob: largest triangle order solved by a TRSM leaf kernel (default 256); larger
  * diagonal tiles recurse (two half solves + a DMMA GEMM update) */
 int bx_set_trsm_leaf(int n);
-/* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16, 32 or 64; default 16) */
+/* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16, 32 or 64; default 32) */
 int bx_set_trsm_rhs(int nr);
 /* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile
  * (default), 2 = persistent 2-SM with double-buffered TMEM accumulators */

@@ -157,7 +157,7 @@ bool need_attr(const void* kernel) {
 
 int g_gemm_variant = 0;  // tuning knob (bx_set_gemm_variant); 0 = default
 int g_gemm_group = 8;    // raster group (m-tiles) of the FP64 task GEMM grid
-int g_trsm_rhs = 16;     // right-hand sides per CTA of the TRSM panel kernel (8/16/32)
+int g_trsm_rhs = 32;     // right-hand sides per CTA of the TRSM panel kernel (8/16/32/64)
 int g_trsm_leaf = 256;   // triangle order solved by a leaf kernel; larger ones recurse
 
 template <class Cfg, bool TA, bool TB>
