@@ -379,7 +379,7 @@ def result_line(args, cfg, val, e2e, peak_measured, clk, cpu, f32, execution="si
         "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
                    "tile": cfg["tile"], "alpha": cfg["alpha"], "beta": cfg["beta"],
                    "l2_flush": "none needed: every step streams > 6 GiB of operands through a 126 MB L2",
-                   "chunk_steps": args.chunk or "auto (GEMM/SYMM 8, others 16)"},
+                   "chunk_steps": args.chunk or "auto (GEMM/SYMM/SYR2K 8, others 16)"},
         "e2e": {"value": e2e["value"], "unit": "TFLOP/s", "ms_per_step": e2e["ms"],
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                 "p2p_bytes_per_step": e2e["p2p"],

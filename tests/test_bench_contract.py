@@ -47,7 +47,7 @@ def test_result_line_has_the_contract_keys():
 @pytest.mark.parametrize("kind,k,ndev,chunk,streams", [
     ("gemm", 1024, 1, 8, 8), ("gemm", 1024, 8, 8, 4), ("symm", 1024, 1, 8, 8),
     ("syrk", 512, 1, 16, 12), ("syrk", 512, 8, 16, 4), ("trsm", 1024, 1, 16, 8),
-    ("trmm", 1024, 1, 16, 8), ("syr2k", 512, 1, 16, 4)])
+    ("trmm", 1024, 1, 16, 8), ("syr2k", 512, 1, 8, 4)])
 def test_auto_launch_shape(kind, k, ndev, chunk, streams):
     # the BASELINE task grids (16 x 16 tiles; K = 16 or 8 steps) at a small element count
     call = build_call(kind, m=1024, n=1024, k=k, tile_size=64, seed=0, uplo="lower",
