@@ -27,6 +27,7 @@ What is different on hardware (SURVEY.md §7 "hard parts" 3-4):
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from collections import deque
@@ -47,6 +48,7 @@ from .program import AxpyOp, GemmOp, MatOp, compile_task, scratch_key
 from .tiling import device_ld
 
 WORKING_SET_TILES = 12   # reference floor (scheduler.py:49-52): 4 tasks x (C + 2 inputs)
+SGEMM_TF32_MIN_K = 512   # auto SGEMM: plain TF32 from this reduction depth up
 LANE_H2D, LANE_D2H, LANE_P2P = -1, -2, -3
 
 
@@ -88,8 +90,9 @@ class RunOptions:
                                        # stream in (-1 = auto, 0 = off; resident mode only)
     defer_c_move_in: bool = True       # beta*C0 added by a final axpy launch, so a task's
                                        # GEMMs do not wait for its C tile (program.py)
-    sgemm_precise: bool = False        # float32 calls: 3xTF32 (fp32 accuracy, 1/3 rate)
-                                       # instead of TF32 inputs (process-wide engine knob)
+    sgemm_precise: Optional[bool] = None   # float32 calls: True = 3xTF32 (fp32 accuracy,
+                                       # 1/3 rate), False = TF32 inputs, None = auto (3xTF32
+                                       # below SGEMM_TF32_MIN_K, sgemm_precise_for)
     critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
                                        # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
@@ -936,9 +939,23 @@ def resolve_ramp(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOpti
     return dataclasses.replace(options, ramp_tasks=ramp if ramp >= 4 else 0)
 
 
+# One call at a time per process: every call carves its tiles out of the process-wide
+# engine's per-GPU arena (offset 0 up) and shares the engine's streams, event pool and
+# singular flag, so concurrent callers (threads, or C callers of libblasx.so with the GIL
+# released inside ctypes) are serialised here.
+_CALL_LOCK = threading.RLock()
+
+
 def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
              options: Optional[RunOptions] = None, engine=None, _t_plan: float = 0.0) -> RunResult:
-    """Execute a task plan on the topology's GPUs; the host output holds the result."""
+    """Execute a task plan on the topology's GPUs; the host output holds the result.
+    Thread-safe: calls from several threads run one after another (``_CALL_LOCK``)."""
+    with _CALL_LOCK:
+        return _run_plan(plan, topology, options, engine, _t_plan)
+
+
+def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[RunOptions],
+              engine, _t_plan: float) -> RunResult:
     from .engine import get_engine
     t_setup0 = time.perf_counter()
     options = options or RunOptions()
@@ -980,22 +997,22 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
                 f"device {d.device_id}: arena of {want} bytes cannot hold the "
                 f"{WORKING_SET_TILES}-tile working set at tile size {plan.tile_size}")
         caps[slot] = want
+    if not all(resident.values()):
+        # one residency mode per call: a resident device copies from a peer's block without
+        # pinning it, which is only safe if that peer can never evict (never reuse) the block
+        resident = {s: False for s in resident}
     engine.ensure_arenas(caps)
     if plan.dtype.itemsize == 4 and hasattr(engine, "lib"):
-        engine.lib.bx_set_sgemm_precise(int(options.sgemm_precise))
-    if plan.snapshot_alias is not None:
+        engine.lib.bx_set_sgemm_precise(int(sgemm_precise_for(plan, options)))
+    if plan.snapshot_alias is not None and not _snapshot_alias_safe(
+            plan, options, topology, devs, resident, caps, per_tile):
+        # the reference's host copy (routines.py:393-400)
+        from .tiling import MatrixDesc as _MD
         snap = plan.matrices[plan.snapshot_alias]
-        snap_bytes = (-(-snap.rows // plan.tile_size) * device_ld(plan.tile_size)
-                      * snap.cols * esz)
-        if (options.execution != "deterministic"
-                or any(snap_bytes + 2 * WORKING_SET_TILES * per_tile > c for c in caps.values())):
-            # cannot keep every snapshot tile resident (or per-GPU threads could race a host
-            # fetch against a write-back): take the reference's host copy
-            from .tiling import MatrixDesc as _MD
-            plan.matrices[plan.snapshot_alias] = _MD(
-                snap.matrix_id, snap.rows, snap.cols, snap.leading_dim, snap.storage.copy(),
-                snap.base_offset)
-            plan.snapshot_alias = None
+        plan.matrices[plan.snapshot_alias] = _MD(
+            snap.matrix_id, snap.rows, snap.cols, snap.leading_dim, snap.storage.copy(),
+            snap.base_offset)
+        plan.snapshot_alias = None
     # Page-lock the operands for the DMA engine.  Buffers pinned by the caller beforehand
     # (``pin_host``; the paper excludes page-locking from timing) stay
     # pinned; the ones pinned here are unpinned when the call returns.
@@ -1044,6 +1061,50 @@ def run_plan(plan: TaskPlan, topology: Optional[Topology] = None,
                       "finalize_s": time.perf_counter() - t_fin0}
     return RunResult(metrics, sorted(rt.trace, key=lambda e: (e.time_start, e.device, e.time_end)),
                      {w.device_id: w.tasks_done for w in workers}, plan)
+
+
+def _snapshot_alias_safe(plan, options, topology, devs, resident, caps, per_tile) -> bool:
+    """TRMM reads its in-place operand through a snapshot (routines.py:393-400).  The
+    snapshot may alias the live storage only if no snapshot tile can be fetched from the
+    host after the task owning it has written it back.  That holds when the owner's own
+    fetch (issued before its write-back) is the tile's only host fetch: every device keeps
+    every tile it fetched (resident arenas, L1 on, room for the whole snapshot), and every
+    other device gets the tile from a holder over L2 (L2 on, one peer group) — with one
+    driver thread, so the directory sees each holder before the next lookup."""
+    if options.execution != "deterministic" or not options.l1_enabled:
+        return False
+    if not all(resident.values()):
+        return False
+    if len(devs) > 1:
+        if not options.l2_enabled:
+            return False
+        if len({topology.peer_group_of(d) for d in devs}) != 1:
+            return False
+    snap = plan.matrices[plan.snapshot_alias]
+    snap_bytes = -(-snap.rows // plan.tile_size) * device_ld(plan.tile_size) * snap.cols * plan.dtype.itemsize
+    return all(snap_bytes + 2 * WORKING_SET_TILES * per_tile <= c for c in caps.values())
+
+
+def sgemm_precise_for(plan: TaskPlan, options: RunOptions) -> bool:
+    """float32 calls: 3xTF32 (fp32-accurate split products) or plain TF32 inputs.
+    ``sgemm_precise=None`` (auto) picks 3xTF32 when the call's reduction depth is below
+    SGEMM_TF32_MIN_K: the TF32 rounding error (2^-11 per input) grows like sqrt(k) while the
+    north-star bound grows like k (k * 2^-23), so plain TF32 meets the fp32 bound only for
+    long reductions."""
+    if options.sgemm_precise is not None:
+        return bool(options.sgemm_precise)
+    env = os.environ.get("BX_SGEMM_PRECISE")
+    if env:
+        return env != "0"
+    return plan.dtype.itemsize == 4 and call_depth(plan.call) < SGEMM_TF32_MIN_K
+
+
+def call_depth(call) -> int:
+    """The reduction depth k of the north-star bound for a routine call."""
+    a = call.a.matrix
+    if call.kind in ("gemm", "syrk", "syr2k"):
+        return a.rows if call.trans_a else a.cols
+    return a.rows      # symm / trmm / trsm: the order of the square operand
 
 
 def _unpin(engine, arrays) -> None:

@@ -665,12 +665,28 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
                 f"execution keeps every tile resident")
         engine.ensure_arenas({slot: want})
     if plan.dtype.itemsize == 4 and hasattr(engine, "lib"):
-        engine.lib.bx_set_sgemm_precise(int(options.sgemm_precise))
+        engine.lib.bx_set_sgemm_precise(int(S.sgemm_precise_for(plan, options)))
     sess.publish_arena(engine, slot)
+    seq = sess.next_call()
+    snap_shm = None
+    if plan.snapshot_alias is not None and not options.l2_enabled:
+        # TRMM snapshot aliasing the live storage is safe only if each snapshot tile is
+        # fetched from the host once, by its first holder, before the owning task writes it
+        # back (the others copy it over L2).  Without L2 every rank fetches on its own:
+        # take the reference's copy (routines.py:393-400), in node-shared memory.
+        from .tiling import MatrixDesc
+        snap = plan.matrices[plan.snapshot_alias]
+        arr = sess.shared_array(f"{seq}_snapshot", int(snap.storage.size), snap.storage.dtype)
+        if r == 0:
+            arr[:] = snap.storage
+        sess.barrier("snapshot copied")
+        snap_shm = sess._shm[-1]
+        plan.matrices[plan.snapshot_alias] = MatrixDesc(
+            snap.matrix_id, snap.rows, snap.cols, snap.leading_dim, arr, snap.base_offset)
+        plan.snapshot_alias = None
     pinned_here = [m.storage for m in plan.matrices.values() if engine.register_host(m.storage)]
 
     tbase, n_tiles = _tile_index(plan)
-    seq = sess.next_call()
     n_tasks = len(plan.tasks)
     blk = None
     if r == 0:
@@ -744,6 +760,15 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
         sess.hdr[5] = 0
         sess.hdr[6] = 0
     sess.barrier("call closed")
+    if snap_shm is not None:
+        try:
+            engine.unregister_host(arr)
+        except Exception:
+            pass
+        sess._shm.remove(snap_shm)
+        sess._arrays.pop()
+        if r == 0:
+            snap_shm.unlink()
     if failed:
         if err is not None and not isinstance(err, _PeerFailed):
             raise err
