@@ -1,23 +1,31 @@
 #!/usr/bin/env python
-"""Benchmark: host-resident tiled DGEMM on B200 (BASELINE.json configs[1]).
+"""Benchmark: host-resident tiled level-3 BLAS on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2|cfg1|dgemm32768|cfg3_syrk|cfg3_syr2k|cfg4_trsm|cfg4_trmm]
+                  [--config cfg2|cfg1|dgemm32768|cfg3_syrk|cfg3_syr2k|cfg4_trsm|cfg4_trmm|cfg5_sgemm]
 
-Prints ONE JSON line (rank 0).  Legs:
-  value     device-resident DGEMM over the same workload (inputs already in HBM; the
-            dominant tile kernel, FP64 DMMA) — whole-job TFLOP/s over the N GPUs;
-  e2e       the public API call (``dgemm`` / ``run_call``) on host-resident numpy buffers,
-            H2D tile loads + D2H write-back inside the timed region — the headline;
-  roofline  dominant kernel: flops per launch / CUDA-event launch time vs the FP64 DMMA
-            peak measured live (MEASURED_PEAKS.json has no FP64 figure);
-  cpu_baseline  the oracle port of the reference tiled runtime (numpy/OpenBLAS, all host
-            cores) on a bounded sample of the same workload.
-Under torchrun (WORLD_SIZE>1) every rank drives its own GPU (LOCAL_RANK) through the
-one-process-per-GPU runtime (spmd.py): shared task queue, stations with stealing, and the
-L2 tile cache over peer HBM via CUDA IPC; steps are bracketed by session barriers and the
-step time is the max over ranks.  ``--gpus N`` without torchrun drives N GPUs from one
-process (the single-address-space runtime).
+Prints ONE JSON line (rank 0).  A "step" is one routine call over the config's seeded
+host-resident operands (BASELINE.json: "host-resident operands").  Legs:
+  value     ``run_call`` (the reference's API, scheduler.py:665-669) on the host buffers:
+            every step plans, loads tiles over the host link (H2D), computes on the FP64
+            tensor cores, writes C back (D2H); timed on the device with CUDA events, max over
+            ranks; whole-job TFLOP/s (plan.total_flops / time);
+  e2e       the cblas-style public API (``dgemm``/``dsyrk``/... on the caller's column-major
+            buffers, blas.py) timed by the host clock around the call, max over ranks, with
+            the H2D/D2H bytes each step moved;
+  roofline  the dominant kernel (the FP64 DMMA task GEMM; tcgen05 TF32 for SGEMM) timed
+            alone on device-resident operands of the config's shape, vs the FP64 DMMA peak
+            measured live (MEASURED_PEAKS.json has no FP64 entry); plus the north-star
+            roofline max(t_tensor, t_link) of the value leg with the host-link / NVLink
+            bandwidths measured in this run with all N GPUs active (``links``);
+  parity    the output of the last timed e2e step checked against the sampled-block oracle
+            (oracle/sampled.py; test infrastructure used as the checker only) with the
+            north-star bound restricted to each block;
+  cpu_baseline  the oracle port of the reference's tiled runtime (numpy + OpenBLAS, all
+            host cores) on sampled output blocks of the same routine and operands.
+``--gpus N``: one process per GPU (spmd.py: shared task queue, stations with stealing, L2
+tile cache over peer HBM through CUDA IPC, no collectives) — under torchrun every rank runs
+this file; without torchrun the script launches the N ranks itself.
 """
 
 from __future__ import annotations
@@ -63,6 +71,8 @@ CONFIGS = {
                             "512-4096 (BASELINE configs[4])"),
 }
 METRIC = "DGEMM TFLOP/s at 1/2/4/8 B200 (host-resident operands), % of FP64 peak"
+METRIC_F32 = "SGEMM TFLOP/s (host-resident operands, tcgen05 kind::tf32), % of TF32 tensor peak"
+PARITY_BLOCKS = {"gemm": 16, "syrk": 16, "syr2k": 16, "trsm": 2, "trmm": 2}
 
 
 def log(*a):
@@ -86,7 +96,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", ",".join(str(g) for g in range(self.gpus))],
+                 "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -163,368 +173,569 @@ def tf32_peak_tflops():
         return 1590.0 / 2.0, "fallback 1.59 PF bf16 / 2 (B200_PROFILING.md)"
 
 
-def cpu_sample(cfg, call, target_s=12.0):
-    """Oracle port of the reference tiled runtime (routines.py:482-492 execute_task_on_host)
-    on sampled output tiles of the same workload, all host threads (OpenBLAS)."""
-    from oracle import tiled
-    a, b, c = (x.matrix.as_2d() for x in (call.a, call.b, call.c))
-    t = cfg["tile"]
-    kt = -(-cfg["k"] // t)
-    tiles = []
-    rng = np.random.default_rng(1)
-    nt = -(-cfg["m"] // t)
-    flops_per_tile = 2 * t * t * cfg["k"]
-    try:   # all host threads, whatever the launcher exported
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(os.cpu_count(), user_api="blas")
-    except Exception:
-        pass
-    # warm-up one tile (OpenBLAS init), then as many tiles as fit target_s
-    tiled.run_tiles_subset("gemm", a, c, b, tile_size=t, tiles=[(0, 0)], alpha=cfg["alpha"],
-                           beta=cfg["beta"])
-    t0 = time.perf_counter()
-    done = 0
-    while time.perf_counter() - t0 < target_s:
-        ij = (int(rng.integers(0, nt)), int(rng.integers(0, nt)))
-        tiled.run_tiles_subset("gemm", a, c, b, tile_size=t, tiles=[ij], alpha=cfg["alpha"],
-                               beta=cfg["beta"])
-        tiles.append(ij)
-        done += 1
-    dt = time.perf_counter() - t0
-    return dict(value=done * flops_per_tile / dt / 1e12, unit="TFLOP/s", cores=os.cpu_count(),
-                kind="port", seconds=dt,
-                sample=f"{done} sampled {t}x{t} output tiles x {kt} k-steps of {cfg['desc']} "
-                       f"({done * flops_per_tile / 1e9:.0f} GFLOP), oracle/tiled.py numpy+OpenBLAS")
+def config_dict(cfg, args):
+    """The ``config`` object — identical for both arms (same routine, shape and scalars)."""
+    return {"workload": cfg["desc"], "routine": cfg["kind"], "m": cfg["m"], "n": cfg["n"],
+            "k": cfg["k"], "tile": cfg["tile"], "alpha": cfg["alpha"], "beta": cfg["beta"],
+            **({"uplo": cfg["uplo"]} if "uplo" in cfg else {}),
+            "dtype": "f32" if cfg.get("dtype") == "f32" else "f64",
+            "operands": "host-resident, column-major, seeded uniform[-1,1) (reference build_call)",
+            "l2_flush": "none needed: every step streams > 2 GiB of operands through a 126 MB L2"}
 
 
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
 
 
-# ----------------------------------------------------------------------------- legs
+def block_flops(kind, blk, cfg):
+    """Algorithmic flops of one sampled output block (plan.total_flops restricted)."""
+    t, k, m, n = cfg["tile"], cfg["k"], cfg["m"], cfg["n"]
+    if kind in ("trsm", "trmm"):
+        if blk[0] == "col":       # side left: an m x w strip against the m x m triangle
+            return float(m) * m * min(t, n - blk[1] * t)
+        return float(n) * n * min(t, m - blk[1] * t)
+    i, j = blk
+    h, w = min(t, m - i * t), min(t, n - j * t)
+    if kind == "gemm":
+        return 2.0 * h * w * k
+    mult = 2.0 if kind == "syr2k" else 1.0
+    return mult * (h * (h + 1) * k if i == j else 2.0 * h * w * k)
+
+
+def cpu_sample(cfg, call, target_s=12.0, seed=1):
+    """The oracle port of the reference tiled runtime (oracle/sampled.py: the same step
+    sequences as routines.py:227-380 run with the kernels.py numerics, execute_task_on_host
+    routines.py:482-492) on random output blocks of this routine and these operands, all
+    host threads (OpenBLAS), for about ``target_s`` seconds."""
+    from oracle import sampled
+    try:   # all host threads, whatever the launcher exported
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count(), user_api="blas")
+    except Exception:
+        pass
+    kind = cfg["kind"]
+    every = sampled.call_blocks(call, 10 ** 6, seed=seed)
+    rng = np.random.default_rng(seed)
+    a = call.a.matrix.as_2d()
+    b = call.b.matrix.as_2d() if call.b is not None else None
+    c = call.c.matrix.as_2d()
+
+    def one(blk):
+        c0 = sampled.snapshot_blocks(c, [blk], cfg["tile"])
+        if kind == "gemm":
+            sampled.check_blocks("gemm", c, c0, a=a, b=b, tile=cfg["tile"], alpha=cfg["alpha"],
+                                 beta=cfg["beta"], eps=1.0)
+        else:
+            sampled.reference_blocks(kind, a, b, c0, tile=cfg["tile"], blocks=[blk],
+                                     alpha=cfg["alpha"], beta=cfg["beta"], uplo=cfg.get("uplo", "upper"))
+    one(every[0])     # warm-up (OpenBLAS thread start)
+    t0 = time.perf_counter()
+    flops, done = 0.0, 0
+    while time.perf_counter() - t0 < target_s or done == 0:
+        blk = every[int(rng.integers(0, len(every)))]
+        one(blk)
+        flops += block_flops(kind, blk, cfg)
+        done += 1
+    dt = time.perf_counter() - t0
+    unit_name = "tile columns" if kind in ("trsm", "trmm") else f"{cfg['tile']}x{cfg['tile']} output tiles"
+    return dict(value=flops / dt / 1e12, unit="TFLOP/s", cores=os.cpu_count(), kind="port",
+                seconds=dt,
+                sample=f"{done} random {unit_name} of {cfg['desc']} ({flops / 1e9:.0f} GFLOP) "
+                       f"with the reference's step sequence, oracle/sampled.py (numpy + OpenBLAS, "
+                       f"{os.cpu_count()} threads)")
+
+
+def api_call(call, options=None, topology=None):
+    """The cblas-style public entry point (blas.py) over the call's column-major buffers."""
+    from paper_1510_05041_b200 import blas
+    a, c = call.a.matrix, call.c.matrix
+    t = call.c.tile_size
+    kw = dict(tile_size=t, options=options, topology=topology)
+    tr = "T" if call.trans_a else "N"
+    up = "U" if call.uplo == "upper" else "L"
+    if call.kind == "gemm":
+        b = call.b.matrix
+        m, n = c.rows, c.cols
+        k = a.rows if call.trans_a else a.cols
+        fn = blas.sgemm if c.storage.dtype == np.float32 else blas.dgemm
+        return fn(tr, "T" if call.trans_b else "N", m, n, k, call.alpha, a.storage, a.leading_dim,
+                  b.storage, b.leading_dim, call.beta, c.storage, c.leading_dim, **kw)
+    if call.kind == "syrk":
+        k = a.rows if call.trans_a else a.cols
+        return blas.dsyrk(up, tr, c.rows, k, call.alpha, a.storage, a.leading_dim, call.beta,
+                          c.storage, c.leading_dim, **kw)
+    if call.kind == "syr2k":
+        b = call.b.matrix
+        k = a.rows if call.trans_a else a.cols
+        return blas.dsyr2k(up, tr, c.rows, k, call.alpha, a.storage, a.leading_dim, b.storage,
+                           b.leading_dim, call.beta, c.storage, c.leading_dim, **kw)
+    fn = blas.dtrsm if call.kind == "trsm" else blas.dtrmm
+    return fn("L" if call.side == "left" else "R", up, tr, "U" if call.diag == "unit" else "N",
+              c.rows, c.cols, call.alpha, a.storage, a.leading_dim, c.storage, c.leading_dim, **kw)
+
+
+def parity_check(call, c0_blocks):
+    """North-star bound on the sampled blocks of the last timed step (oracle/sampled.py)."""
+    from oracle import sampled, tolerance
+    t0 = time.perf_counter()
+    worst, per = sampled.call_check(call, c0_blocks)
+    eps = float(np.finfo(call.c.matrix.storage.dtype).eps)
+    return {"max_ratio": worst, "bound": tolerance.BOUND, "pass": bool(worst <= tolerance.BOUND),
+            "blocks": len(per),
+            "block_kind": "tile columns (independent sub-problems)" if call.kind in ("trsm", "trmm")
+            else f"{call.c.tile_size}x{call.c.tile_size} output tiles",
+            "eps": eps, "checked": "output of the last timed e2e step vs oracle/sampled.py "
+                                   "(reference step sequence), bound restricted to each block",
+            "seconds": time.perf_counter() - t0}
+
+
+# ----------------------------------------------------------------------------- reference arm
 
 def run_reference(args, cfg):
-    call = make_operands(CONFIGS["cfg2"] if cfg["kind"] != "gemm" else cfg, seed=0)
-    cfg_g = cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"]
+    """The reference's CPU path (oracle port of its tiled runtime, all host cores) on the
+    same routine, operands and scalars; each step is a bounded sample of the workload."""
+    call = make_operands(cfg, seed=0)
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(cfg_g, call, target_s=args.ref_seconds)
+        r = cpu_sample(cfg, call, target_s=args.ref_seconds, seed=1 + i)
         if i >= args.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
     sec = statistics.median([r["seconds"] for r in vals])
-    return {"metric": METRIC, "value": v, "unit": "TFLOP/s", "impl": "reference",
+    return {"metric": METRIC_F32 if cfg.get("dtype") == "f32" else METRIC, "value": v,
+            "unit": "TFLOP/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1))",
-            "config": {"workload": cfg_g["desc"], "m": cfg_g["m"], "n": cfg_g["n"], "k": cfg_g["k"],
-                       "tile": cfg_g["tile"]},
+            "vs_baseline": None, "dtype": "f32" if cfg.get("dtype") == "f32" else "f64",
+            "data": "synthetic (seeded uniform[-1,1), reference build_call generator)",
+            "config": config_dict(cfg, args),
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": vals[0]["cores"],
                              "kind": "port", "sample": vals[0]["sample"]},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def device_value_leg(args, cfg, eng, lib, N):
-    """Device-resident DGEMM of the same shape, sharded by column panels over the GPUs."""
+# ----------------------------------------------------------------------------- kernel leg
+
+def kernel_shape(cfg):
+    """(m, n, k) of the device-resident launch of the dominant kernel: the config's own GEMM
+    shape; for the rank-k / triangular routines the GEMM their tasks are made of."""
+    if cfg["kind"] in ("syrk", "syr2k"):
+        return cfg["n"], cfg["n"], cfg["k"]
+    if cfg["kind"] in ("trsm", "trmm"):
+        return cfg["m"], cfg["n"], cfg["m"]
+    return cfg["m"], cfg["n"], cfg["k"]
+
+
+def kernel_leg(args, cfg, eng, lib, slot, cols, seed, sync_all=None):
+    """The dominant kernel alone: one device-resident launch per step over this GPU's column
+    panel, timed with CUDA events on the launching stream (compute lane 0)."""
     from paper_1510_05041_b200 import _native as NN
-    m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    m, _, k = kernel_shape(cfg)
     f32 = cfg.get("dtype") == "f32"
     esz = 4 if f32 else 8
-    ngpu = args.gpus
-    cols = [n // ngpu + (1 if g < n % ngpu else 0) for g in range(ngpu)]
-    bufs = []
-    for g in range(ngpu):
-        slot = eng.slot(g)
-        ptrs = []
-        for nelem in (m * k, k * cols[g], m * cols[g]):
-            p = C.c_uint64()
-            NN.check(lib.bx_dev_alloc(slot, nelem * esz, C.byref(p)), "alloc")
-            if f32:
-                NN.check(lib.bx_dev_fill_uniform_f32(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
-            else:
-                NN.check(lib.bx_dev_fill_uniform(slot, p.value, nelem, 1234 + len(ptrs), 0), "fill")
-            ptrs.append(p.value)
-        bufs.append(ptrs)
-    for g in range(ngpu):
-        eng.device_sync(eng.slot(g))
+    ptrs = []
+    for i, nelem in enumerate((m * k, k * cols, m * cols)):
+        p = C.c_uint64()
+        NN.check(lib.bx_dev_alloc(slot, nelem * esz, C.byref(p)), "alloc")
+        fill = lib.bx_dev_fill_uniform_f32 if f32 else lib.bx_dev_fill_uniform
+        NN.check(fill(slot, p.value, nelem, seed + i, 0), "fill")
+        ptrs.append(p.value)
+    eng.device_sync(slot)
+    a, b, c = ptrs
 
-    def launch(g):
-        s = eng.slot(g)
-        a, b, c = bufs[g]
+    def launch():
         if f32:
-            NN.check(lib.bx_sgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 0.0, c, m), "sgemm")
+            NN.check(lib.bx_sgemm_device(slot, 0, 0, 0, m, cols, k, 1.0, a, m, b, k, 0.0, c, m), "sgemm")
         else:
-            NN.check(lib.bx_dgemm_device(s, 0, 0, 0, m, cols[g], k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
-
-    for _ in range(args.warmup):
-        for g in range(ngpu):
-            launch(g)
-    for g in range(ngpu):
-        eng.device_sync(eng.slot(g))
-    per_launch = []
-    evs = []
+            NN.check(lib.bx_dgemm_device(slot, 0, 0, 0, m, cols, k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
+    for _ in range(max(1, min(args.warmup, 3))):
+        launch()
+    eng.device_sync(slot)
     n0 = eng.launches()
-    t_steps = []
-    for _ in range(args.steps):
-        pairs = []
-        for g in range(ngpu):
-            s = eng.slot(g)
-            e0 = eng.record(s, 0, timing=True)
-            launch(g)
-            e1 = eng.record(s, 0, timing=True)
-            pairs.append((s, e0, e1))
-        step_ms = 0.0
-        for s, e0, e1 in pairs:
-            eng.sync(e1)
-            ms = eng.elapsed_ms(e0, e1)
-            per_launch.append((ms, 2.0 * m * cols[s] * k))
-            step_ms = max(step_ms, ms)
-            eng.release(e0)
-            eng.release(e1)
-        t_steps.append(step_ms)
-    launches = eng.launches() - n0
-    for g in range(ngpu):
-        s = eng.slot(g)
-        for p in bufs[g]:
-            lib.bx_dev_free(s, p)
-    ms_step = statistics.mean(t_steps)
-    flops = 2.0 * m * n * k
-    avg_launch_ms = statistics.mean(x[0] for x in per_launch)
-    avg_launch_flops = statistics.mean(x[1] for x in per_launch)
-    return dict(value=flops / (ms_step / 1e3) / 1e12, ms_per_step=ms_step, launches=launches,
-                kernel_tflops=avg_launch_flops / (avg_launch_ms / 1e3) / 1e12,
-                avg_launch_ms=avg_launch_ms, flops_per_launch=avg_launch_flops)
-
-
-def e2e_leg(args, cfg, eng):
-    from paper_1510_05041_b200 import RunOptions, run_call
-    from paper_1510_05041_b200.devices import DeviceDesc, Topology
-    call = make_operands(cfg, seed=0)
-    topo = Topology([DeviceDesc(g, peer_group="nvlink") for g in range(args.gpus)])
-    opts = RunOptions(chunk_steps=args.chunk, n_streams=args.streams,
-                      tasks_per_stream=args.tasks_per_stream)
-    for m in (call.a, call.b, call.c):
-        if m is not None:
-            eng.register_host(m.matrix.storage)   # page-locking excluded from timing (PAPER.md:720)
-    res = None
-    for _ in range(args.warmup):
-        res = run_call(call, topo, opts)
-    times, metrics = [], []
-    n0 = eng.launches()
-    for _ in range(args.steps):
-        e0 = eng.record(0, 0, timing=True)
-        res = run_call(call, topo, opts)
-        e1 = eng.record(0, 0, timing=True)
+    times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        if sync_all:
+            sync_all()
+        e0 = eng.record(slot, 0, timing=True)
+        launch()
+        e1 = eng.record(slot, 0, timing=True)
         eng.sync(e1)
         times.append(eng.elapsed_ms(e0, e1))
         eng.release(e0)
         eng.release(e1)
-        metrics.append(res.metrics)
     launches = eng.launches() - n0
+    for p in ptrs:
+        lib.bx_dev_free(slot, p)
     ms = statistics.mean(times)
-    flops = res.plan.total_flops
-    mt = metrics[-1]
+    fl = 2.0 * m * cols * k
+    return dict(ms=ms, flops=fl, tflops=fl / (ms / 1e3) / 1e12, launches=launches,
+                shape=[m, cols, k])
+
+
+# ----------------------------------------------------------------------------- links
+
+def link_probe(eng, lib, slot, nbytes=256 << 20, reps=4, peers=None, sync_all=None):
+    """Pinned host->device / device->host bandwidth of this GPU's copy lanes (one 2-d tile
+    copy of ``nbytes`` into/out of the arena, the engine's own bx_h2d_tile / bx_d2h_tile),
+    timed with events on the copy lane; ``sync_all`` (a cross-GPU barrier) makes every GPU
+    copy at once, so the figures are per-GPU bandwidths with N GPUs active.  ``peers``:
+    [(src_ptr or slot, kind)] for the peer-to-peer figure (CUDA IPC or cudaMemcpyPeer)."""
+    from paper_1510_05041_b200.engine import LANE_D2H, LANE_H2D, LANE_P2P
+    rows = 8192
+    cols = max(1, nbytes // (rows * 8))
+    nbytes = rows * cols * 8
+    if eng.arena_capacity(slot) < 2 * nbytes:
+        return None
+    host = np.empty(rows * cols, dtype=np.float64)
+    host[:] = 1.0
+    eng.register_host(host)
+
+    class _Desc:      # the h2d/d2h wrappers take a MatrixDesc-like source
+        leading_dim = rows
+        itemsize = 8
+
+        @staticmethod
+        def element_address(r, c):
+            return host.ctypes.data + 8 * (r + c * rows)
+    out = {}
+    try:
+        for name, lane in (("h2d", LANE_H2D), ("d2h", LANE_D2H)):
+            ts = []
+            for _ in range(reps):
+                if sync_all:
+                    sync_all()
+                e0 = eng.record(slot, lane, timing=True)
+                if name == "h2d":
+                    ev = eng.h2d(slot, 0, rows, _Desc, 0, 0, rows, cols)
+                else:
+                    ev = eng.d2h(slot, 0, rows, _Desc, 0, 0, rows, cols)
+                e1 = eng.record(slot, lane, timing=True)
+                eng.sync(e1)
+                ts.append(eng.elapsed_ms(e0, e1))
+                for e in (ev, e0, e1):
+                    eng.release(e)
+            out[name + "_gbs"] = nbytes / (min(ts) / 1e3) / 1e9
+        if peers:
+            ts = []
+            for _ in range(reps):
+                if sync_all:
+                    sync_all()
+                e0 = eng.record(slot, LANE_P2P, timing=True)
+                evs = []
+                for src, kind in peers:
+                    if kind == "ipc":
+                        evs.append(eng.copy_remote(slot, nbytes, src, nbytes))
+                    else:
+                        evs.append(eng.p2p(slot, nbytes, src, 0, nbytes))
+                e1 = eng.record(slot, LANE_P2P, timing=True)
+                eng.sync(e1)
+                ts.append(eng.elapsed_ms(e0, e1))
+                for e in evs + [e0, e1]:
+                    eng.release(e)
+            out["p2p_in_gbs"] = len(peers) * nbytes / (min(ts) / 1e3) / 1e9
+    finally:
+        eng.unregister_host(host)
+    out["bytes_per_copy"] = nbytes
+    return out
+
+
+# ----------------------------------------------------------------------------- the line
+
+def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parity,
+                execution="single process"):
+    """The bench JSON line (shared by the single-process and one-process-per-GPU paths)."""
+    f32 = cfg.get("dtype") == "f32"
+    n = args.gpus
+    flops = val["flops"]
+    peak_tf, peak_src = peak_measured, ("measured live: register-only DMMA.8x8x4 loop "
+                                        "(bx_fp64_peak_probe); MEASURED_PEAKS.json has no FP64 entry")
+    if f32:
+        peak_tf, peak_src = tf32_peak_tflops()
+    # north-star roofline: slower of aggregate tensor time and the bytes this run moved over
+    # the host links / NVLink at the bandwidths measured in this run with all N GPUs active
+    t_tensor = flops / (n * peak_tf * 1e12)
+    t_link = None
+    if links and links.get("h2d_gbs"):
+        per_dev = val["per_device"]
+        h2d_max = max(d["h2d"] for d in per_dev.values())
+        p2p_max = max(d["d2d_in"] for d in per_dev.values())
+        t_link = h2d_max / (links["h2d_gbs"] * 1e9)
+        if p2p_max:
+            t_link += p2p_max / (links["p2p_in_gbs"] * 1e9) if links.get("p2p_in_gbs") else float("nan")
+    t_meas = val["ms"] / 1e3
+    roof = max(t_tensor, t_link or 0.0)
+    out = {
+        "metric": METRIC_F32 if f32 else METRIC,
+        "value": val["value"], "unit": "TFLOP/s",
+        "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": val["ms"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (tf32 MMA, f32 accumulate)" if f32 else "f64",
+        "data": "synthetic: seeded uniform[-1,1) host operands (reference build_call generator); "
+                "device-filled uniform[-1,1) for the kernel-alone roofline leg",
+        "config": config_dict(cfg, args),
+        "frac_of_tensor_peak": val["value"] / (n * peak_tf),
+        "e2e": {"value": e2e["value"], "unit": "TFLOP/s", "ms_per_step": e2e["ms"],
+                "api": e2e["api"],
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                "p2p_bytes_per_step": e2e["p2p"]},
+        "cache": {"h2d_bytes": val["h2d"], "p2p_bytes": val["p2p"], "d2h_bytes": val["d2h"],
+                  "l1_hits": val["l1"], "l2_hits": val["l2"], "host_fetches": val["host"],
+                  "per_device": val["per_device"]},
+        "roofline": {"bound": "tensor", "achieved": kern["tflops"], "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": kern["tflops"] / peak_tf,
+                     "traffic": kern.get("traffic"),
+                     "kernel": ("bx::sgemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 "
+                                "pair tile, TMEM accumulators, TMA)" if f32 else
+                                "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
+                     "kernel_shape": kern["shape"], "flops_per_launch": kern["flops"],
+                     "avg_launch_ms": kern["ms"], "peak_source": peak_src,
+                     "fp64_dmma_peak_measured": peak_measured,
+                     "north_star": {"t_tensor_s": t_tensor, "t_link_s": t_link,
+                                    "t_measured_s": t_meas, "frac": roof / t_meas,
+                                    "bound": "link" if (t_link or 0) > t_tensor else "tensor",
+                                    "links_measured": links}},
+        "parity": parity,
+        "gpu_launches": val["launches"] + e2e["launches"] + kern["launches"],
+        "gpu_launches_detail": {"value_leg": val["launches"], "e2e_leg": e2e["launches"],
+                                "kernel_leg": kern["launches"]},
+        **({"tile_sweep": val["sweep"]} if val.get("sweep") else {}),
+        "clocks": clk.summary() if clk else None,
+        "execution": execution,
+    }
+    if cpu:
+        out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    return out
+
+
+def _metrics_summary(res):
+    mt = res.metrics
+    return dict(h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(), p2p=mt.total_d2d_bytes(),
+                l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
+                per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
+                            for d, v in mt.devices.items()})
+
+
+# ----------------------------------------------------------------------------- one process
+
+def single_bench(args, cfg):
+    """N GPUs driven from this process (the reference's shape; N=1 by default)."""
+    from paper_1510_05041_b200 import RunOptions, _native as NN, run_call
+    from paper_1510_05041_b200.devices import DeviceDesc, Topology
+    from paper_1510_05041_b200.engine import get_engine
+    from oracle import sampled
+    lib = NN.load()
+    NN.require_gpu()
+    eng = get_engine(list(range(args.gpus)), 4)
+    peak = C.c_double()
+    NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
+    call = make_operands(cfg, seed=0)
+    topo = Topology([DeviceDesc(g, peer_group="nvlink") for g in range(args.gpus)])
+    opts = RunOptions(chunk_steps=args.chunk, n_streams=args.streams,
+                      tasks_per_stream=args.tasks_per_stream)
+    for mt in (call.a, call.b, call.c):
+        if mt is not None:
+            eng.register_host(mt.matrix.storage)   # page-locking excluded (PAPER.md:720-721)
+    for _ in range(args.warmup):
+        run_call(call, topo, opts)
+    slots = [eng.slot(g) for g in range(args.gpus)]
+    links = link_probe(eng, lib, slots[0],
+                       peers=[(s, "peer") for s in slots[1:]] if len(slots) > 1 else None)
+
+    def all_sync():
+        for s in slots:
+            eng.device_sync(s)
+
+    with ClockSampler(list(range(args.gpus))) as clk:
+        # value: run_call (RoutineCall API), device-event timed
+        n0 = eng.launches()
+        times = []
+        res = None
+        for _ in range(args.steps):
+            all_sync()
+            e0 = eng.record(slots[0], 0, timing=True)
+            res = run_call(call, topo, opts)
+            e1 = eng.record(slots[0], 0, timing=True)
+            eng.sync(e1)
+            all_sync()
+            times.append(eng.elapsed_ms(e0, e1))
+            eng.release(e0)
+            eng.release(e1)
+        v_launch = eng.launches() - n0
+        ms = statistics.mean(times)
+        val = dict(value=res.plan.total_flops / (ms / 1e3) / 1e12, ms=ms, flops=res.plan.total_flops,
+                   launches=v_launch, **_metrics_summary(res))
+        # e2e: the cblas-style public API, host clock
+        blocks = sampled.call_blocks(call, PARITY_BLOCKS[cfg["kind"]], seed=1)
+        n0 = eng.launches()
+        wall = []
+        c0 = None
+        for s in range(args.steps):
+            if s == args.steps - 1:
+                c0 = sampled.call_snapshot(call, blocks)
+            all_sync()
+            t0 = time.perf_counter()
+            r2 = api_call(call, opts, topo)
+            wall.append((time.perf_counter() - t0) * 1e3)
+        e_launch = eng.launches() - n0
+        ms2 = statistics.mean(wall)
+        ms_e2e = _metrics_summary(r2)
+        e2e = dict(value=r2.plan.total_flops / (ms2 / 1e3) / 1e12, ms=ms2, launches=e_launch,
+                   api=f"blas.{ 's' if cfg.get('dtype') == 'f32' else 'd'}{cfg['kind']} (cblas-style, "
+                       f"caller's column-major host buffers)", **ms_e2e)
+        kern = kernel_leg(args, cfg, eng, lib, slots[0], kernel_shape(cfg)[1], 1234)
+    parity = parity_check(call, c0)
     sweep = []
     for t in cfg.get("sweep", ()):
         c2 = retile(call, t)
         run_call(c2, topo, opts)
-        e0 = eng.record(0, 0, timing=True)
-        r2 = run_call(c2, topo, opts)
-        e1 = eng.record(0, 0, timing=True)
+        all_sync()
+        e0 = eng.record(slots[0], 0, timing=True)
+        r3 = run_call(c2, topo, opts)
+        e1 = eng.record(slots[0], 0, timing=True)
         eng.sync(e1)
         tms = eng.elapsed_ms(e0, e1)
         eng.release(e0)
         eng.release(e1)
-        m2 = r2.metrics
-        sweep.append(dict(tile=t, ms=tms, tflops=flops / (tms / 1e3) / 1e12,
-                          h2d_bytes=m2.total_h2d_bytes(), p2p_bytes=m2.total_d2d_bytes(),
-                          d2h_bytes=m2.total_d2h_bytes(), tasks=len(r2.plan.tasks),
-                          l1_hits=m2.l1_hits, l2_hits=m2.l2_hits, host_fetches=m2.host_fetches))
-    return dict(value=flops / (ms / 1e3) / 1e12, ms=ms, flops=flops, launches=launches, sweep=sweep,
-                h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(), p2p=mt.total_d2d_bytes(),
-                l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
-                per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
-                            for d, v in mt.devices.items()}, call=call)
-
-
-def result_line(args, cfg, val, e2e, peak_measured, clk, cpu, f32, execution="single process"):
-    """The bench JSON line (shared by the single-process and one-process-per-GPU paths)."""
-    flops = e2e["flops"]
-    h2d_bw, p2p_bw = 53.0e9, 700e9      # measured (profiles/peaks_r01.json); P2P: nominal-measured
-    peak_tf = peak_measured
-    peak_src = ("measured live: register-only DMMA.8x8x4 loop (bx_fp64_peak_probe); "
-                "MEASURED_PEAKS.json has no FP64 entry")
-    if f32:
-        peak_tf, peak_src = tf32_peak_tflops()
-    t_a = flops / (args.gpus * peak_tf * 1e12)
-    t_b = e2e["h2d"] / (h2d_bw * args.gpus) + e2e["p2p"] / (p2p_bw * args.gpus)
-    prof = os.path.join(ROOT, "profiles", "ncu_dgemm_traffic_r01.json")
-    traffic = None
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
-    kernel_tf = val["kernel_tflops"] if val else e2e["value"]
-    out = {
-        "metric": METRIC if not f32 else "SGEMM TFLOP/s (host-resident operands, tcgen05 kind::tf32), % of TF32 tensor peak",
-        "value": val["value"] if val else e2e["value"],
-        "unit": "TFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": val["ms_per_step"] if val else e2e["ms"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (tf32 MMA, f32 accumulate)" if f32 else "f64",
-        "data": "synthetic: seeded uniform[-1,1) (reference build_call generator) for e2e; "
-                "device-filled uniform[-1,1) for the HBM-resident leg",
-        "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
-                   "tile": cfg["tile"], "alpha": cfg["alpha"], "beta": cfg["beta"],
-                   "l2_flush": "none needed: every step streams > 6 GiB of operands through a 126 MB L2",
-                   "chunk_steps": args.chunk or "auto (GEMM/SYMM/SYR2K 8, others 16)"},
-        "e2e": {"value": e2e["value"], "unit": "TFLOP/s", "ms_per_step": e2e["ms"],
-                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
-                "p2p_bytes_per_step": e2e["p2p"],
-                "frac_of_tensor_peak": e2e["value"] / (args.gpus * peak_tf),
-                "cache": {"l1_hits": e2e["l1"], "l2_hits": e2e["l2"], "host_fetches": e2e["host"]},
-                "per_device": e2e["per_device"],
-                "roofline_north_star": {"t_tensor_s": t_a, "t_link_s": t_b,
-                                        "frac": max(t_a, t_b) / (e2e["ms"] / 1e3),
-                                        "h2d_gbs_assumed": h2d_bw / 1e9, "p2p_gbs_assumed": p2p_bw / 1e9}},
-        "roofline": {"bound": "tensor", "achieved": kernel_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": kernel_tf / peak_tf, "traffic": None if f32 else traffic,
-                     "kernel": ("bx::sgemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 pair tile, TMEM accumulators, TMA)"
-                                if f32 else "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
-                     "peak_source": peak_src,
-                     "fp64_dmma_peak_measured": peak_measured,
-                     "flops_per_launch": val["flops_per_launch"] if val else None,
-                     "avg_launch_ms": val["avg_launch_ms"] if val else None},
-        "gpu_launches": e2e["launches"] + (val["launches"] if val else 0),
-        **({"tile_sweep": e2e["sweep"]} if e2e["sweep"] else {}),
-        "gpu_launches_e2e": e2e["launches"],
-        "clocks": clk.summary(),
-    }
-    if cpu:
-        out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    out["execution"] = execution
-    return out
+        m3 = r3.metrics
+        sweep.append(dict(tile=t, ms=tms, tflops=r3.plan.total_flops / (tms / 1e3) / 1e12,
+                          h2d_bytes=m3.total_h2d_bytes(), p2p_bytes=m3.total_d2d_bytes(),
+                          d2h_bytes=m3.total_d2h_bytes(), tasks=len(r3.plan.tasks),
+                          l1_hits=m3.l1_hits, l2_hits=m3.l2_hits, host_fetches=m3.host_fetches))
+    val["sweep"] = sweep
+    cpu = None if args.no_cpu_baseline else cpu_sample(cfg, call, target_s=args.cpu_seconds)
+    line = result_line(args, cfg, val, e2e, kern, peak.value, clk, cpu, links, parity,
+                       execution=f"single process, {args.gpus} GPU(s)")
+    print(json.dumps(line), flush=True)
+    return line
 
 
 # ----------------------------------------------------------------------------- one process per GPU
 
 def spmd_bench(args, cfg):
-    """WORLD_SIZE > 1 (torchrun): every rank drives its own GPU (LOCAL_RANK) through the SPMD
-    runtime (paper_1510_05041_b200/spmd.py: shared task queue, stations with stealing, IPC
-    peer tile cache).  Each step is bracketed by a session barrier and a device sync on
-    every rank; the step time is the max over ranks of the rank's CUDA-event time."""
+    """One process per GPU (torchrun, or ``launch_ranks``): every rank drives its own GPU
+    through the SPMD runtime (paper_1510_05041_b200/spmd.py).  Each step is bracketed by a
+    session barrier and a device sync on every rank; step time = max over ranks of each
+    rank's CUDA-event time.  Returns rank 0's line (None elsewhere)."""
     from paper_1510_05041_b200 import RunOptions, run_call, spmd
     from paper_1510_05041_b200 import _native as NN
     from paper_1510_05041_b200.engine import get_engine
-    # --ranks-share-gpu: every rank on GPU 0 (exercises the multi-process path on a 1-GPU box)
+    from oracle import sampled
     sess = spmd.init(device=0 if args.ranks_share_gpu else None)
     r, W = sess.rank, sess.world
     lib = NN.load()
     NN.require_gpu()
-    f32 = cfg.get("dtype") == "f32"
     eng = get_engine([r], 4, [sess.device])
     slot = eng.slot(r)
     peak = C.c_double()
     NN.check(lib.bx_fp64_peak_probe(slot, 40000, C.byref(peak)), "peak probe")
     peak_v = float(sess.allgather(peak.value).min())
 
-    def timed(fn):
+    def barrier_sync():
         sess.barrier("step start")
         eng.device_sync(slot)
-        e0 = eng.record(slot, 0, timing=True)
-        out = fn()
-        e1 = eng.record(slot, 0, timing=True)
-        eng.sync(e1)
-        eng.device_sync(slot)
-        ms = eng.elapsed_ms(e0, e1)
-        eng.release(e0)
-        eng.release(e1)
-        return sess.allreduce_max(ms), ms, out
 
-    clk = ClockSampler(W) if r == 0 else None
+    call = make_operands(cfg, seed=0) if r == 0 else None
+    call = sess.share_call(call)
+    for mt in (call.a, call.b, call.c):
+        if mt is not None:
+            eng.register_host(mt.matrix.storage)   # page-locking excluded from timing
+    opts = RunOptions(execution="spmd", chunk_steps=args.chunk, n_streams=args.streams,
+                      tasks_per_stream=args.tasks_per_stream)
+    for _ in range(args.warmup):
+        run_call(call, options=opts)
+    # links with all ranks active: H2D/D2H of this rank's lanes, P2P from the next rank's
+    # arena over CUDA IPC (a ring: every GPU reads one peer at once)
+    bases = sess.peer_bases(eng, slot)
+    nxt = (r + 1) % W
+    links = link_probe(eng, lib, slot, peers=[(bases[nxt], "ipc")] if W > 1 else None,
+                       sync_all=lambda: sess.barrier("link probe"))
+    if links:
+        agg = {k: float(sess.allgather(links.get(k) or 0.0).min()) for k in ("h2d_gbs", "d2h_gbs", "p2p_in_gbs")}
+        links.update(agg)
+        links["note"] = "per GPU, minimum over ranks, all ranks copying at once"
+
+    clk = ClockSampler([sess.device] if args.ranks_share_gpu else list(range(W))) if r == 0 else None
     if clk:
         clk.__enter__()
     try:
-        val = None
-        if cfg["kind"] == "gemm":
-            m, n, k = cfg["m"], cfg["n"], cfg["k"]
-            esz = 4 if f32 else 8
-            cols = [n // W + (1 if g < n % W else 0) for g in range(W)]
-            mine = cols[r]
-            ptrs = []
-            for i, nelem in enumerate((m * k, k * mine, m * mine)):
-                p = C.c_uint64()
-                NN.check(lib.bx_dev_alloc(slot, nelem * esz, C.byref(p)), "alloc")
-                fill = lib.bx_dev_fill_uniform_f32 if f32 else lib.bx_dev_fill_uniform
-                NN.check(fill(slot, p.value, nelem, 1234 + 7 * r + i, 0), "fill")
-                ptrs.append(p.value)
-            eng.device_sync(slot)
-            a, b, c = ptrs
-
-            def launch():
-                if f32:
-                    NN.check(lib.bx_sgemm_device(slot, 0, 0, 0, m, mine, k, 1.0, a, m, b, k, 0.0, c, m), "sgemm")
-                else:
-                    NN.check(lib.bx_dgemm_device(slot, 0, 0, 0, m, mine, k, 1.0, a, m, b, k, 1.0, c, m), "dgemm")
-            for _ in range(args.warmup):
-                launch()
-            n0 = eng.launches()
-            steps, mine_ms = [], []
-            for _ in range(args.steps):
-                t, own, _ = timed(launch)
-                steps.append(t)
-                mine_ms.append(own)
-            launches = int(sess.allgather(eng.launches() - n0).sum())
-            for p in ptrs:
-                lib.bx_dev_free(slot, p)
-            ms_step = statistics.mean(steps)
-            own_ms = statistics.mean(mine_ms)
-            flops_mine = 2.0 * m * mine * k
-            # dominant-kernel roofline: rank-average launch time and flops
-            avg_ms = float(sess.allgather(own_ms).mean())
-            avg_fl = float(sess.allgather(flops_mine).mean())
-            val = dict(value=2.0 * m * n * k / (ms_step / 1e3) / 1e12, ms_per_step=ms_step,
-                       launches=launches, kernel_tflops=avg_fl / (avg_ms / 1e3) / 1e12,
-                       avg_launch_ms=avg_ms, flops_per_launch=avg_fl)
-
-        call = make_operands(cfg, seed=0) if r == 0 else None
-        call = sess.share_call(call)
-        for mt in (call.a, call.b, call.c):
-            if mt is not None:
-                eng.register_host(mt.matrix.storage)   # page-locking excluded from timing
-        opts = RunOptions(execution="spmd", chunk_steps=args.chunk, n_streams=args.streams,
-                          tasks_per_stream=args.tasks_per_stream)
-        res = None
-        for _ in range(args.warmup):
-            res = run_call(call, options=opts)
         n0 = eng.launches()
         times = []
+        res = None
         for _ in range(args.steps):
-            t, _, res = timed(lambda: run_call(call, options=opts))
-            times.append(t)
-        launches = int(sess.allgather(eng.launches() - n0).sum())
+            barrier_sync()
+            e0 = eng.record(slot, 0, timing=True)
+            res = run_call(call, options=opts)
+            e1 = eng.record(slot, 0, timing=True)
+            eng.sync(e1)
+            eng.device_sync(slot)
+            times.append(sess.allreduce_max(eng.elapsed_ms(e0, e1)))
+            eng.release(e0)
+            eng.release(e1)
+        v_launch = int(sess.allgather(eng.launches() - n0).sum())
+        ms = statistics.mean(times)
+        val = dict(value=res.plan.total_flops / (ms / 1e3) / 1e12, ms=ms, flops=res.plan.total_flops,
+                   launches=v_launch, **_metrics_summary(res))
+        # e2e: the public run_call in spmd mode on the shared host buffers, host clock
+        blocks = sampled.call_blocks(call, PARITY_BLOCKS[cfg["kind"]], seed=1) if r == 0 else None
+        n0 = eng.launches()
+        wall = []
+        c0 = None
+        r2 = None
+        for s in range(args.steps):
+            if s == args.steps - 1 and r == 0:
+                c0 = sampled.call_snapshot(call, blocks)
+            barrier_sync()
+            t0 = time.perf_counter()
+            r2 = run_call(call, options=opts)
+            wall.append(sess.allreduce_max((time.perf_counter() - t0) * 1e3))
+        e_launch = int(sess.allgather(eng.launches() - n0).sum())
+        ms2 = statistics.mean(wall)
+        e2e = dict(value=r2.plan.total_flops / (ms2 / 1e3) / 1e12, ms=ms2, launches=e_launch,
+                   api="run_call(call, options=RunOptions(execution='spmd')) on node-shared host "
+                       "buffers, every rank", **_metrics_summary(r2))
+        m, n, k = kernel_shape(cfg)
+        cols = [n // W + (1 if g < n % W else 0) for g in range(W)]
+        kern = kernel_leg(args, cfg, eng, lib, slot, cols[r], 1234 + 7 * r,
+                          sync_all=lambda: sess.barrier("kernel step"))
+        kern["tflops"] = float(sess.allgather(kern["tflops"]).mean())
+        kern["launches"] = int(sess.allgather(kern["launches"]).sum())
     finally:
         if clk:
             clk.__exit__(None, None, None)
-    ms = statistics.mean(times)
-    mt = res.metrics
-    e2e = dict(value=res.plan.total_flops / (ms / 1e3) / 1e12, ms=ms, flops=res.plan.total_flops,
-               launches=launches, sweep=[], h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(),
-               p2p=mt.total_d2d_bytes(), l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
-               per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
-                           for d, v in mt.devices.items()})
-    sess.barrier("bench end")
+    line = None
     if r == 0:
-        line = result_line(args, cfg, val, e2e, peak_v, clk, None, f32,
+        parity = parity_check(call, c0)
+        line = result_line(args, cfg, val, e2e, kern, peak_v, clk, None, links, parity,
                            execution=f"one process per GPU ({W} ranks, spmd runtime)")
-        print(json.dumps(line), flush=True)
-    sess.barrier("bench printed")
+        if not args.no_cpu_baseline and W == 1:
+            line["cpu_baseline"] = {k: v for k, v in cpu_sample(cfg, call, args.cpu_seconds).items()
+                                    if k in ("value", "unit", "cores", "kind", "sample")}
+    sess.barrier("bench end")
     spmd.shutdown()
+    return line
 
 
-def main():
+def _rank_main(argv):
+    """Entry point of a rank started by ``launch_ranks`` (module-level: spawn imports it)."""
+    args = parse_args(argv)
+    line = spmd_bench(args, CONFIGS_FOR(args))
+    return line
+
+
+def launch_ranks(args, argv):
+    """``--gpus N`` without torchrun: start one process per GPU (spmd.launch) running the
+    same bench, and print rank 0's line."""
+    import bench as this      # importable by name in the spawned ranks (ROOT is on sys.path)
+    from paper_1510_05041_b200 import spmd
+    devices = [0] * args.gpus if args.ranks_share_gpu else list(range(args.gpus))
+    outs = spmd.launch(args.gpus, this._rank_main, argv, devices=devices, timeout=3600)
+    print(json.dumps(outs[0]), flush=True)
+
+
+# ----------------------------------------------------------------------------- main
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -535,54 +746,47 @@ def main():
     ap.add_argument("--streams", type=int, default=0)
     ap.add_argument("--tasks-per-stream", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--single-process", action="store_true",
+                    help="--gpus N>1 from one process (the reference's shape) instead of N ranks")
     ap.add_argument("--ranks-share-gpu", action="store_true",
-                    help="torchrun test mode: all ranks use GPU 0 (numbers are not scaling)")
+                    help="N ranks all on GPU 0 (functional check of the multi-process path)")
     ap.add_argument("--tile", type=int, default=0, help="override the config's tile size")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    args.steps = max(1, args.steps)
+    return args
+
+
+def CONFIGS_FOR(args):
     cfg = CONFIGS[args.config]
     if args.tile:
         cfg = dict(cfg, tile=args.tile, desc=cfg["desc"].replace(f"tile {cfg['tile']}", f"tile {args.tile}"))
+    return cfg
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
+    cfg = CONFIGS_FOR(args)
     rank, world = dist_env()
-    if args.gpus != world and world > 1:
+    if world > 1 and args.gpus != world:
         log(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
         args.gpus = world
-
     if args.impl == "reference":
         # the reference's CPU path: rank 0 alone runs it, the other ranks exit without work
         if rank == 0:
             print(json.dumps(run_reference(args, cfg)), flush=True)
         return
-
     if world > 1:
-        spmd_bench(args, cfg)
+        line = spmd_bench(args, cfg)
+        if line is not None:
+            print(json.dumps(line), flush=True)
         return
-
-    from paper_1510_05041_b200 import _native as NN
-    from paper_1510_05041_b200.engine import get_engine
-    lib = NN.load()
-    NN.require_gpu()
-    f32 = cfg.get("dtype") == "f32"
-    eng = get_engine(list(range(args.gpus)), 4)
-    if os.environ.get("BX_TRSM_LEAF"):
-        NN.check(lib.bx_set_trsm_leaf(int(os.environ["BX_TRSM_LEAF"])), "trsm leaf")
-    peak = C.c_double()
-    NN.check(lib.bx_fp64_peak_probe(0, 40000, C.byref(peak)), "peak probe")
-
-    with ClockSampler(args.gpus) as clk:
-        if cfg["kind"] == "gemm":
-            val = device_value_leg(args, cfg, eng, lib, NN)
-        else:
-            val = None
-        e2e = e2e_leg(args, cfg, eng)
-
-    cpu = None
-    if not args.no_cpu_baseline:
-        cpu = cpu_sample(cfg if cfg["kind"] == "gemm" else CONFIGS["cfg2"],
-                         e2e["call"] if cfg["kind"] == "gemm" else make_operands(CONFIGS["cfg2"]),
-                         target_s=10.0)
-
-    print(json.dumps(result_line(args, cfg, val, e2e, peak.value, clk, cpu, f32)), flush=True)
+    if args.gpus > 1 and not args.single_process:
+        launch_ranks(args, argv)
+        return
+    single_bench(args, cfg)
 
 
 if __name__ == "__main__":

@@ -26,22 +26,71 @@ class _Clk:
         return {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": [], "samples": 3}
 
 
+def _legs():
+    per_dev = {"0": dict(h2d=6.44e9, d2d_in=0, tasks=256)}
+    val = dict(value=34.9, ms=252.0, flops=8.8e12, launches=1536, h2d=6.44e9, d2h=2.15e9, p2p=0,
+               l1=7680, l2=0, host=512, per_device=per_dev)
+    e2e = dict(value=34.5, ms=255.0, launches=1536, api="blas.dgemm", h2d=6.44e9, d2h=2.15e9,
+               p2p=0, l1=7680, l2=0, host=512, per_device=per_dev)
+    kern = dict(ms=246.0, flops=8.8e12, tflops=35.7, launches=3, shape=[16384, 16384, 16384])
+    cpu = dict(value=0.45, unit="TFLOP/s", cores=16, kind="port", sample="x", seconds=10.0)
+    links = {"h2d_gbs": 53.0, "d2h_gbs": 54.0, "bytes_per_copy": 1 << 28}
+    parity = {"max_ratio": 0.01, "bound": 10.0, "pass": True, "blocks": 16}
+    return val, e2e, kern, cpu, links, parity
+
+
 def test_result_line_has_the_contract_keys():
     args = types.SimpleNamespace(gpus=1, steps=3, warmup=3, chunk=0)
     cfg = bench.CONFIGS["cfg2"]
-    val = dict(value=35.7, ms_per_step=246.0, launches=3, kernel_tflops=35.7, avg_launch_ms=246.0,
-               flops_per_launch=8.8e12)
-    e2e = dict(value=34.8, ms=252.0, flops=8.8e12, launches=1536, sweep=[], h2d=6.44e9, d2h=2.15e9,
-               p2p=0, l1=7680, l2=0, host=512, per_device={"0": dict(h2d=6.44e9, d2d_in=0, tasks=256)})
-    cpu = dict(value=0.45, unit="TFLOP/s", cores=16, kind="port", sample="x", seconds=10.0)
-    line = bench.result_line(args, cfg, val, e2e, 37.1, _Clk(), cpu, False)
+    val, e2e, kern, cpu, links, parity = _legs()
+    line = bench.result_line(args, cfg, val, e2e, kern, 37.1, _Clk(), cpu, links, parity)
     json.dumps(line)
     assert [k for k in REQUIRED if k not in line] == []
+    # value = the host-resident run_call (the BASELINE metric), not the kernel alone
+    assert line["value"] == 34.9 and line["ms_per_step"] == 252.0
     assert line["e2e"]["h2d_bytes_per_step"] == 6.44e9 and line["e2e"]["unit"] == "TFLOP/s"
     r = line["roofline"]
     assert r["bound"] == "tensor" and r["frac"] == pytest.approx(35.7 / 37.1)
+    ns = r["north_star"]
+    assert ns["t_link_s"] == pytest.approx(6.44e9 / 53e9)
+    assert ns["frac"] == pytest.approx(max(ns["t_tensor_s"], ns["t_link_s"]) / 0.252)
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 16
     assert line["higher_is_better"] is True and line["vs_baseline"] is None
+    assert line["parity"]["pass"] and line["gpu_launches"] == 1536 * 2 + 3
+
+
+def test_reference_arm_reports_the_same_config():
+    """Both arms describe the same routine, shape and scalars (same_config)."""
+    args = types.SimpleNamespace(gpus=1, steps=3, warmup=3, chunk=0)
+    for name in ("cfg2", "cfg3_syrk", "cfg4_trsm"):
+        cfg = bench.CONFIGS[name]
+        val, e2e, kern, cpu, links, parity = _legs()
+        ours = bench.result_line(args, cfg, val, e2e, kern, 37.1, _Clk(), cpu, links, parity)
+        assert ours["config"] == bench.config_dict(cfg, args)
+        assert "alpha" in ours["config"] and "beta" in ours["config"]
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3_syrk", "cfg3_syr2k", "cfg4_trsm", "cfg4_trmm"])
+def test_cpu_sample_runs_the_configs_routine(name, monkeypatch):
+    """The CPU baseline / reference arm samples blocks of the config's OWN routine (small
+    shape here), and counts their algorithmic flops."""
+    cfg = dict(bench.CONFIGS[name], m=256, n=256, k=256 if name != "cfg3_syrk" else 128, tile=64)
+    call = bench.make_operands(cfg, seed=0)
+    r = bench.cpu_sample(cfg, call, target_s=0.05)
+    assert r["value"] > 0 and r["kind"] == "port"
+    unit = "tile columns" if cfg["kind"] in ("trsm", "trmm") else "output tiles"
+    assert unit in r["sample"]
+
+
+def test_block_flops_sum_to_plan_flops():
+    from oracle import sampled
+    from paper_1510_05041_b200.routines import generate_tasks
+    for name in ("cfg2", "cfg3_syrk", "cfg3_syr2k", "cfg4_trsm", "cfg4_trmm"):
+        cfg = dict(bench.CONFIGS[name], m=300, n=300, k=200, tile=64)
+        call = bench.make_operands(cfg, seed=0)
+        blocks = sampled.call_blocks(call, 10 ** 6)
+        total = sum(bench.block_flops(cfg["kind"], b, cfg) for b in blocks)
+        assert total == pytest.approx(generate_tasks(call).total_flops, rel=1e-12), name
 
 
 @pytest.mark.parametrize("kind,k,ndev,chunk,streams", [

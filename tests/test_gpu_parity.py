@@ -245,15 +245,20 @@ def _sgemm_case(ta, tb, m, n, k):
 
 
 def test_cblas_sgemm():
+    """The cblas-style sgemm at a short reduction (k = 100: auto 3xTF32) meets the north-
+    star bound with the float32 epsilon."""
     from paper_1510_05041_b200 import sgemm
     rng = np.random.default_rng(4)
-    m, n, k = 700, 600, 500
+    m, n, k = 700, 600, 100
     a = np.asfortranarray(rng.random((m, k), dtype=np.float32))
     b = np.asfortranarray(rng.random((k, n), dtype=np.float32))
     c = np.asfortranarray(np.zeros((m, n), dtype=np.float32))
     sgemm("N", "N", m, n, k, 1.0, a, m, b, k, 0.0, c, m, tile_size=256)
-    ref = a.astype(np.float64) @ b.astype(np.float64)
-    assert np.linalg.norm(c - ref) / np.linalg.norm(ref) < 1e-3
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    r = tolerance.gemm_ratio(c, a64 @ b64, a_norm=np.linalg.norm(a64), b_norm=np.linalg.norm(b64),
+                             k=k, alpha=1.0, beta=0.0, c0_norm=0.0,
+                             eps=float(np.finfo(np.float32).eps))
+    assert r <= tolerance.BOUND, r
 
 
 VIRTUAL = [100, 101, 102]   # logical devices sharing GPU 0 (own streams, events, arenas)
@@ -359,30 +364,50 @@ def test_randomized_routines_against_oracle(case):
         assert tolerance.trsm_residual_ratio(tri, out, c0, alpha, side, EPS) <= tolerance.BOUND
 
 
-@pytest.mark.parametrize("i", range(12))
+def _sgemm_ratio(call, t, alpha, beta, ta, tb, k, opts):
+    a = call.a.matrix.as_2d().astype(np.float64)
+    b = call.b.matrix.as_2d().astype(np.float64)
+    c0 = call.c.matrix.as_2d().astype(np.float64)
+    run_call(call, options=opts)
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=t, alpha=alpha, beta=beta, trans_a=ta, trans_b=tb)
+    return tolerance.gemm_ratio(call.c.matrix.as_2d().astype(np.float64), ref,
+                                a_norm=np.linalg.norm(a), b_norm=np.linalg.norm(b), k=k,
+                                alpha=alpha, beta=beta, c0_norm=np.linalg.norm(c0),
+                                eps=float(np.finfo(np.float32).eps))
+
+
+@pytest.mark.parametrize("i", range(24))
 def test_randomized_sgemm_against_fp64_oracle(i):
-    """Random ragged SGEMM calls (tcgen05 kind::tf32) vs the float64 oracle.  The MMA rounds
-    its inputs to TF32 (10-bit mantissa): relative to a bound with the fp32 epsilon
-    (2^-23) the error ratio falls like k^-1.5, so the fp32-epsilon bound holds from k ~ 200
-    (and at every BASELINE shape) while small k is held to the TF32 unit roundoff 2^-11."""
+    """Random ragged SGEMM calls with the default (auto) precision vs the float64 oracle,
+    held to the north-star bound with the float32 epsilon (2^-23) at every k: calls whose
+    reduction is shorter than SGEMM_TF32_MIN_K run 3xTF32, longer ones plain TF32."""
     rng = np.random.default_rng(500 + i)
-    m, n, k = (int(x) for x in rng.integers(1, 900, size=3))
+    m, n = (int(x) for x in rng.integers(1, 900, size=2))
+    k = int(rng.integers(1, 1400))
     ta, tb = bool(rng.integers(2)), bool(rng.integers(2))
     t = int(rng.choice([128, 256, 512]))
     alpha, beta = float(rng.choice([1.0, -0.5])), float(rng.choice([0.0, 1.0]))
     call = build_call("gemm", m=m, n=n, k=k, tile_size=t, seed=i, alpha=alpha, beta=beta,
                       trans_a=ta, trans_b=tb, dtype=np.float32)
-    a = call.a.matrix.as_2d().astype(np.float64)
-    b = call.b.matrix.as_2d().astype(np.float64)
-    c0 = call.c.matrix.as_2d().astype(np.float64)
-    run_call(call, options=RunOptions(chunk_steps=int(rng.choice([1, 16]))))
-    ref = c0.copy()
-    tiled.run_tiled("gemm", a, ref, b, tile_size=t, alpha=alpha, beta=beta, trans_a=ta, trans_b=tb)
-    eps = float(np.finfo(np.float32).eps) if k >= 256 else 2.0 ** -11
-    r = tolerance.gemm_ratio(call.c.matrix.as_2d().astype(np.float64), ref, a_norm=np.linalg.norm(a),
-                             b_norm=np.linalg.norm(b), k=k, alpha=alpha, beta=beta,
-                             c0_norm=np.linalg.norm(c0), eps=eps)
+    r = _sgemm_ratio(call, t, alpha, beta, ta, tb, k,
+                     RunOptions(chunk_steps=int(rng.choice([1, 16]))))
     assert r <= tolerance.BOUND, (r, k)
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_plain_tf32_meets_fp32_bound_from_crossover(i):
+    """The crossover itself: plain TF32 (forced) at reduction depths just above
+    SGEMM_TF32_MIN_K already meets the float32-epsilon bound."""
+    from paper_1510_05041_b200.scheduler import SGEMM_TF32_MIN_K
+    rng = np.random.default_rng(700 + i)
+    m, n = int(rng.integers(64, 900)), int(rng.integers(64, 900))
+    k = int(rng.integers(SGEMM_TF32_MIN_K, SGEMM_TF32_MIN_K + 128))
+    ta, tb = bool(rng.integers(2)), bool(rng.integers(2))
+    call = build_call("gemm", m=m, n=n, k=k, tile_size=256, seed=40 + i, alpha=1.0, beta=1.0,
+                      trans_a=ta, trans_b=tb, dtype=np.float32)
+    r = _sgemm_ratio(call, 256, 1.0, 1.0, ta, tb, k, RunOptions(sgemm_precise=False))
+    assert r <= tolerance.BOUND / 2, (r, k)
 
 
 @pytest.mark.parametrize("i", range(6))
