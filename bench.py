@@ -221,13 +221,9 @@ def cpu_sample(cfg, call, target_s=12.0, seed=1):
     c = call.c.matrix.as_2d()
 
     def one(blk):
-        c0 = sampled.snapshot_blocks(c, [blk], cfg["tile"])
-        if kind == "gemm":
-            sampled.check_blocks("gemm", c, c0, a=a, b=b, tile=cfg["tile"], alpha=cfg["alpha"],
-                                 beta=cfg["beta"], eps=1.0)
-        else:
-            sampled.reference_blocks(kind, a, b, c0, tile=cfg["tile"], blocks=[blk],
-                                     alpha=cfg["alpha"], beta=cfg["beta"], uplo=cfg.get("uplo", "upper"))
+        c0 = sampled.snapshot_blocks(c, [blk], cfg["tile"])[blk]
+        sampled.compute_block(kind, a, b, c0, blk, tile=cfg["tile"], alpha=cfg["alpha"],
+                              beta=cfg["beta"], uplo=cfg.get("uplo", "upper"))
     one(every[0])     # warm-up (OpenBLAS thread start)
     t0 = time.perf_counter()
     flops, done = 0.0, 0

@@ -100,6 +100,17 @@ int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, i
 int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h,
                  int w, double alpha, uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait,
                  const int* wait, int* ev_out);
+/* inverse-based TRSM diagonal step (kernels.py:105-161 restated as X = alpha inv(E) B):
+ * inv (n x n) = inv(E), E = op(tri(A)) of the diagonal tile, by the substitution solve
+ * E Z = I (same division rule and singular flag as bx_trsm_tile); computed once per
+ * diagonal tile and reused by every task of that tile row (left) / column (right) */
+int bx_trsm_inverse(int dev, int stream, int upper, int trans, int unit, int n, uint64_t a_off,
+                    int lda, uint64_t inv_off, int ldi, int n_wait, const int* wait, int* ev_out);
+/* x (h x w) = alpha inv(E) B (left) / alpha B inv(E) (right); eff_upper = upper ^ trans;
+ * the FP64 task GEMM reading only the k-range where the triangular inv(E) is non-zero */
+int bx_trsm_apply(int dev, int stream, int side_right, int eff_upper, int h, int w, double alpha,
+                  uint64_t inv_off, int ldi, uint64_t b_off, int ldb, uint64_t x_off, int ldx,
+                  int n_wait, const int* wait, int* ev_out);
 /* dst (n x n) = op(tri(A)) [mode 0, unit diag substituted] or sym(A) [mode 1] */
 int bx_materialize(int dev, int stream, int mode_sym, int upper, int trans, int unit, int n,
                    uint64_t a_off, int lda, uint64_t dst_off, int ldd, int n_wait, const int* wait,

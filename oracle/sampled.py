@@ -174,6 +174,24 @@ class _Grid:
         self.rows, self.cols = _ceil(m, t), _ceil(n, t)
 
 
+def compute_block(kind, a, b, c0_block, blk, *, tile, alpha, beta, trans_a=False, trans_b=False,
+                  uplo="upper", side="left", diag="non-unit"):
+    """One block's reference result, nothing else (the CPU-baseline timer's unit of work);
+    GEMM works on the tile's own panels, widened to float64 panel by panel."""
+    if kind == "gemm":
+        m = a.shape[1] if trans_a else a.shape[0]
+        n = b.shape[0] if trans_b else b.shape[1]
+        r, c = _rows(blk, tile, m), _cols(blk, tile, n)
+        a_sub = np.asarray(a[:, r] if trans_a else a[r, :], np.float64)
+        b_sub = np.asarray(b[c, :] if trans_b else b[:, c], np.float64)
+        return reference_blocks("gemm", a_sub, b_sub, {(0, 0): np.asarray(c0_block, np.float64)},
+                                tile=tile, blocks=[(0, 0)], alpha=alpha, beta=beta,
+                                trans_a=trans_a, trans_b=trans_b)[(0, 0)]
+    return reference_blocks(kind, a, b, {blk: c0_block}, tile=tile, blocks=[blk], alpha=alpha,
+                            beta=beta, trans_a=trans_a, trans_b=trans_b, uplo=uplo, side=side,
+                            diag=diag)[blk]
+
+
 # ---- per-block bound ------------------------------------------------------------------
 
 def block_ratio(kind, blk, got, ref, c0, *, a, b, tile, alpha, beta, eps, trans_a=False,

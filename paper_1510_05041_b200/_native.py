@@ -53,6 +53,8 @@ _SIGS = {
     "bx_gemm_task_packed": [_i, _i, _i, _i, _i, _i, _i, _i, _i, _p, _d, _d, _u64, _i, _i, _pi, _pi],
     "bx_sgemm_device": [_i, _i, _i, _i, _i, _i, _i, C.c_float, _u64, _i, _u64, _i, C.c_float, _u64, _i],
     "bx_trsm_tile": [_i, _i, _i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _i, _pi, _pi],
+    "bx_trsm_inverse": [_i, _i, _i, _i, _i, _i, _u64, _i, _u64, _i, _i, _pi, _pi],
+    "bx_trsm_apply": [_i, _i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_materialize": [_i, _i, _i, _i, _i, _i, _i, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_axpy_tile": [_i, _i, _i, _i, _i, _d, _u64, _i, _u64, _i, _i, _pi, _pi],
     "bx_singular_flag": [_i, _i, _pi],

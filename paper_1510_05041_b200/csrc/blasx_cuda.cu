@@ -483,7 +483,7 @@ int gemm_tma(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
 
 int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, const double* const* a,
              const int* lda, const double* const* b, const int* ldb, const int* depth, double alpha,
-             double beta, double* c, int ldc) {
+             double beta, double* c, int ldc, int kmode = bx::KM_NONE) {
   if (h < 0 || w < 0 || nsteps < 0) return set_err(BX_EINVAL, "gemm: negative extent");
   if (ldc < (h > 1 ? h : 1)) return set_err(BX_EINVAL, "gemm: ldc < h");
   for (int i = 0; i < nsteps; ++i) {
@@ -509,6 +509,7 @@ int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
     t.beta = (s0 == 0) ? beta : 1.0;
     int n = nsteps - s0 < bx::G_MAX_STEPS ? nsteps - s0 : bx::G_MAX_STEPS;
     t.nsteps = n;
+    t.kmode = (nsteps == 1) ? kmode : bx::KM_NONE;
     for (int i = 0; i < n; ++i) {
       t.steps[i].a = a[s0 + i]; t.steps[i].b = b[s0 + i];
       t.steps[i].lda = lda[s0 + i]; t.steps[i].ldb = ldb[s0 + i]; t.steps[i].d = depth[s0 + i];
@@ -569,8 +570,6 @@ int trsm_leaf(cudaStream_t s, int right, int eff_upper, int trans, int unit, int
     case 64: { int rc = launch_panel<64>(s, t); if (rc) return rc; break; }
     default: { int rc = launch_panel<16>(s, t); if (rc) return rc; break; }
   }
-  g_launches++;
-  CUDA_TRY(cudaGetLastError());
   return BX_OK;
 }
 
@@ -625,6 +624,11 @@ int trsm_rec(cudaStream_t s, int right, int eff_upper, int trans, int unit, int 
   int d = n2;
   if ((rc = gemm_raw(s, 0, trans, 0, h, n1, 1, (const double* const*)&b2, &ldb, &e21, &lda, &d, -1.0, 1.0, b1, ldb))) return rc;
   return trsm_rec(s, 1, 0, trans, unit, h, n1, 1.0, e11, lda, b1, ldb, flag, leaf_max);
+}
+
+__global__ void identity_kernel(double* __restrict__ p, int ld, int n) {
+  const int r = blockIdx.x * 32 + threadIdx.x, c = blockIdx.y * 8 + threadIdx.y;
+  if (r < n && c < n) p[(size_t)c * ld + r] = (r == c) ? 1.0 : 0.0;
 }
 
 __global__ void fill_uniform_f32_kernel(float* p, uint64_t n, uint64_t seed) {
@@ -965,6 +969,65 @@ int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int 
   int eff_upper = (upper != 0) != (trans != 0);
   rc = trsm_rec(s, side_right, eff_upper, trans, unit, h, w, alpha, (const double*)(D->arena + a_off), lda,
                 (double*)(D->arena + b_off), ldb, D->flag_dev, g_trsm_leaf);
+  if (rc) return rc;
+  return finish(dev, s, ev_out);
+}
+
+// Inverse of a diagonal tile's triangle for the inverse-based TRSM diagonal step:
+// inv(E), E = op(tri(A)) of order n, by the substitution solve E Z = I (the same kernels
+// and division rule as bx_trsm_tile, so an exact zero on a non-unit diagonal raises the
+// singular flag).  Z has exact zeros outside E's triangle.
+int bx_trsm_inverse(int dev, int stream, int upper, int trans, int unit, int n, uint64_t a_off, int lda,
+                    uint64_t inv_off, int ldi, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  if (n <= 0 || lda < n || ldi < n || (lda & 1) || (ldi & 1)) return set_err(BX_EINVAL, "trsm inverse: bad extents");
+  if (inv_off + (uint64_t)ldi * n * 8 > D->arena_bytes || a_off + (uint64_t)lda * (n - 1) * 8 + 8 * n > D->arena_bytes)
+    return set_err(BX_EINVAL, "trsm inverse: outside arena");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  double* z = (double*)(D->arena + inv_off);
+  dim3 blk(32, 8), grd((n + 31) / 32, (n + 7) / 8);
+  identity_kernel<<<grd, blk, 0, s>>>(z, ldi, n);
+  g_launches++;
+  CUDA_TRY(cudaGetLastError());
+  const int eff_upper = (upper != 0) != (trans != 0);
+  rc = trsm_rec(s, 0, eff_upper, trans, unit, n, n, 1.0, (const double*)(D->arena + a_off), lda, z, ldi, D->flag_dev,
+                g_trsm_leaf);
+  if (rc) return rc;
+  return finish(dev, s, ev_out);
+}
+
+// The TRSM diagonal step with a precomputed inverse: X = alpha inv(E) B (left) or
+// X = alpha B inv(E) (right) into a separate tile x, on the FP64 task GEMM with the
+// triangular-operand k-range (each CTA reads only where inv(E) can be non-zero).
+int bx_trsm_apply(int dev, int stream, int side_right, int eff_upper, int h, int w, double alpha, uint64_t inv_off,
+                  int ldi, uint64_t b_off, int ldb, uint64_t x_off, int ldx, int n_wait, const int* wait, int* ev_out) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  cudaStream_t s = lane_stream(D, stream);
+  if (!s || stream < 0) return set_err(BX_EINVAL, "bad compute stream");
+  const int n = side_right ? w : h;
+  if (h <= 0 || w <= 0 || ldi < n || ldb < h || ldx < h) return set_err(BX_EINVAL, "trsm apply: bad extents");
+  if (x_off + (uint64_t)ldx * w * 8 > D->arena_bytes || b_off + (uint64_t)ldb * w * 8 > D->arena_bytes ||
+      inv_off + (uint64_t)ldi * n * 8 > D->arena_bytes)
+    return set_err(BX_EINVAL, "trsm apply: outside arena");
+  if (x_off == b_off) return set_err(BX_EINVAL, "trsm apply: the result must not alias B");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  int rc = wait_all(s, n_wait, wait);
+  if (rc) return rc;
+  const double* inv = (const double*)(D->arena + inv_off);
+  const double* bp = (const double*)(D->arena + b_off);
+  double* x = (double*)(D->arena + x_off);
+  if (!side_right)
+    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &inv, &ldi, &bp, &ldb, &n, alpha, 0.0, x, ldx,
+                  eff_upper ? bx::KM_A_UPPER : bx::KM_A_LOWER);
+  else
+    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &bp, &ldb, &inv, &ldi, &n, alpha, 0.0, x, ldx,
+                  eff_upper ? bx::KM_B_UPPER : bx::KM_B_LOWER);
   if (rc) return rc;
   return finish(dev, s, ev_out);
 }

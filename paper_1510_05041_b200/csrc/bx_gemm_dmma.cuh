@@ -26,6 +26,10 @@ namespace bx {
 constexpr int G_MAX_STEPS = 40;
 
 enum TriMode { TRI_NONE = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
+// Triangular operand (one-step tasks): a CTA reads only the k-range where the triangular
+// operand can be non-zero — e.g. X = inv(L) B with inv(L) lower: output row block
+// [m0, m0+BM) needs k < m0+BM — halving the flops of a TRSM diagonal-tile apply.
+enum KMode { KM_NONE = 0, KM_A_LOWER = 1, KM_A_UPPER = 2, KM_B_UPPER = 3, KM_B_LOWER = 4 };
 
 struct GemmStep {
   const double* a;
@@ -35,7 +39,7 @@ struct GemmStep {
 
 struct GemmTask {
   double* c;
-  int ldc, h, w, nsteps, tri, group_m;
+  int ldc, h, w, nsteps, tri, group_m, kmode;
   double alpha, beta;
   GemmStep steps[G_MAX_STEPS];
 };
@@ -337,6 +341,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
     total += (t.steps[s].d + BK - 1) / BK;
     kfull = kfull && (t.steps[s].d % BK == 0);
   }
+  // triangular operand (one step): this CTA's k-range; kbeg is a multiple of BM or BN
+  int kbeg = 0, kend = -1;
+  if (t.kmode != KM_NONE && t.nsteps == 1) {
+    const int d = t.steps[0].d;
+    kend = d;
+    if (t.kmode == KM_A_LOWER) kend = min(d, m0 + BM);
+    else if (t.kmode == KM_A_UPPER) kbeg = m0;
+    else if (t.kmode == KM_B_UPPER) kend = min(d, n0 + BN);
+    else kbeg = n0;
+    total = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  }
   // Interior CTAs (no tile edge in m, n or any step's k) take an unpredicated cp.async
   // path with no bounds arithmetic; edge CTAs keep the zero-filling path.
   const bool bulk = kfull && m0 + BM <= t.h && n0 + BN <= t.w && !Cfg::NOLOAD;
@@ -348,7 +363,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   }
   __syncthreads();
 
-  int ld_step = 0, ld_k = 0;
+  int ld_step = 0, ld_k = kbeg;
   auto produce = [&](int slab) {
     const int stage = slab % STAGES;
     if (slab >= STAGES) mbar_wait(&empty[stage], ((slab / STAGES) - 1) & 1);
@@ -365,7 +380,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
       cp_async_arrive_noinc(&full[stage]);
     }
     ld_k += BK;
-    if (ld_k >= st.d) { ld_k = 0; ++ld_step; }
+    if (ld_k >= (kend >= 0 ? kend : st.d)) { ld_k = 0; ++ld_step; }
   };
   for (int s = 0; s < DIST && s < total; ++s) produce(s);
 

@@ -189,6 +189,23 @@ class CudaEngine:
                                       C.byref(ev)), "trsm tile")
         return ev.value
 
+    def trsm_inverse(self, slot, stream, upper, trans, unit, n, a_off, lda, inv_off, ldi,
+                     waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_trsm_inverse(slot, stream, int(upper), int(trans), int(unit), n, a_off,
+                                         lda, inv_off, ldi, nw, wp, C.byref(ev)), "trsm inverse")
+        return ev.value
+
+    def trsm_apply(self, slot, stream, right, eff_upper, h, w, alpha, inv_off, ldi, b_off, ldb,
+                   x_off, ldx, waits=()) -> int:
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_trsm_apply(slot, stream, int(right), int(eff_upper), h, w, float(alpha),
+                                       inv_off, ldi, b_off, ldb, x_off, ldx, nw, wp, C.byref(ev)),
+                "trsm apply")
+        return ev.value
+
     def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
                     waits=()) -> int:
         ev = C.c_int(-1)

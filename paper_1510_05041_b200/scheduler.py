@@ -96,6 +96,9 @@ class RunOptions:
     critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
                                        # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
+    trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
+                                       # (resident arenas): X = alpha inv(E) B with inv(E)
+                                       # computed once per diagonal tile; 0 = substitution
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -283,6 +286,8 @@ class _GpuWorker:
                                       and runtime.topology.peer_group_of(d) == grp)
         self._one_group = len(self._group_peers) == len(runtime.topology.devices) - 1
         self._pending_keys = set()   # resident blocks whose arrival event is not known done
+        self._inv = {}               # diagonal tile key -> [offset, ld, event, landed]
+        self._inv_events = []
 
     # ---- cache callbacks ------------------------------------------------------------
 
@@ -751,10 +756,24 @@ class _GpuWorker:
                     ao, al, aw = res[op.key]
                     waits = ([aw] if aw is not None else []) + act.pending_waits
                     act.pending_waits = []
-                    ev = self._timed(stream, lambda wt, op=op, ao=ao, al=al: eng.trsm(
-                        slot, stream, call.side == "right", call.uplo == "upper", call.trans_a,
-                        call.diag == "unit", h, w, op.alpha, ao, al, act.c_off, act.c_ld, wt),
-                        waits, "KERNEL", op.flops, op.k)
+                    inv = self._trsm_inverse(op.key, ao, al, aw, stream, w if call.side == "right" else h)
+                    if inv is not None:
+                        # X = alpha inv(E) B into a fresh tile, which becomes the task's C
+                        inv_off, inv_ld, inv_wait = inv
+                        x_off = self.cache.allocate_under_pressure(act.c_ld * w * self.esz, self)
+                        eff_upper = (call.uplo == "upper") != call.trans_a
+                        ev = self._timed(stream, lambda wt, op=op, x_off=x_off: eng.trsm_apply(
+                            slot, stream, call.side == "right", eff_upper, h, w, op.alpha, inv_off,
+                            inv_ld, act.c_off, act.c_ld, x_off, act.c_ld, wt),
+                            waits + ([inv_wait] if inv_wait is not None else []), "KERNEL",
+                            op.flops, op.k)
+                        act.scratch.append(act.c_off)
+                        act.c_off = x_off
+                    else:
+                        ev = self._timed(stream, lambda wt, op=op, ao=ao, al=al: eng.trsm(
+                            slot, stream, call.side == "right", call.uplo == "upper", call.trans_a,
+                            call.diag == "unit", h, w, op.alpha, ao, al, act.c_off, act.c_ld, wt),
+                            waits, "KERNEL", op.flops, op.k)
                     self._launched(act, ev)
                     break
             act.next_op = i
@@ -775,6 +794,33 @@ class _GpuWorker:
             return True
         finally:
             self._cur = None
+
+    def _trsm_inverse(self, key, a_off, a_ld, a_wait, stream, n):
+        """inv(E) of the diagonal tile ``key`` for the inverse-based TRSM diagonal step
+        (resident arenas only): computed once per GPU and call by the first task that needs
+        it, on that task's stream; later tasks wait on its event.  Returns (offset, ld,
+        event to wait on or None), or None for the substitution path."""
+        opts = self.runtime.options
+        if (not self.resident or self.f32 or not opts.trsm_inverse_min
+                or n < opts.trsm_inverse_min):
+            return None
+        ent = self._inv.get(key)
+        if ent is None:
+            ld = device_ld(n)
+            try:
+                off = self.arena.alloc(ld * n * self.esz)
+            except ArenaOutOfMemoryError:
+                return None
+            call = self.plan.call
+            ev = self._timed(stream, lambda wt: self.eng.trsm_inverse(
+                self.slot, stream, call.uplo == "upper", call.trans_a, call.diag == "unit", n,
+                a_off, a_ld, off, ld, wt), [a_wait] if a_wait is not None else [], "KERNEL",
+                n * n * n // 3, -1)
+            self._inv_events.append(ev)
+            self._inv[key] = ent = [off, ld, ev, False]
+        if not ent[3] and self.eng.done(ent[2]):
+            ent[3] = True
+        return ent[0], ent[1], None if ent[3] else ent[2]
 
     # ---- completion -----------------------------------------------------------------
 
@@ -830,6 +876,11 @@ class _GpuWorker:
         return all(a is None for a in self.active)
 
     def release_all(self) -> None:
+        for off, _ld, _ev, _landed in self._inv.values():
+            self.arena.free(off)
+        for ev in self._inv_events:
+            self.eng.release(ev)
+        self._inv, self._inv_events = {}, []
         if self._permanent:
             self.cache.release(self._permanent)
             self._permanent = []
@@ -899,6 +950,8 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
     per_tile = device_ld(t) * t * esz
     slots = options.n_streams * options.tasks_per_stream + max(0, options.ramp_tasks)
     want += (slots + 2) * 2 * per_tile + (64 << 20)
+    if plan.call.kind == "trsm" and options.trsm_inverse_min:
+        want += -(-plan.call.a.matrix.rows // t) * per_tile      # one inverse per diagonal tile
     if free_bytes is None:
         return want
     cap = int(free_bytes * 0.9) - (1 << 30)

@@ -46,7 +46,7 @@ class FakeEngine:
         self.ops_log = []
         self._lock = threading.RLock()
         for name in ("ensure_arenas", "register_host", "unregister_host", "h2d", "d2h", "p2p",
-                     "gemm", "trsm", "materialize", "singular", "record", "done", "wait_any",
+                     "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
                      "sync", "stream_wait", "device_sync"):
             setattr(self, name, _locked(getattr(type(self), name)).__get__(self))
 
@@ -193,6 +193,33 @@ class FakeEngine:
                              bool(trans))
             except O.OracleSingular:
                 self.flag[slot] = True
+        return self._enqueue(slot, stream, fn, waits)
+
+    def trsm_inverse(self, slot, stream, upper, trans, unit, n, a_off, lda, inv_off, ldi, waits=()):
+        self.n_launches += 1
+
+        def fn():
+            a = self._view(slot, a_off, lda, n, n).copy()
+            z = np.eye(n)
+            try:
+                O.trsm_solve(z, a, 1.0, "upper" if upper else "lower",
+                             "unit" if unit else "non-unit", "left", bool(trans))
+            except O.OracleSingular:
+                self.flag[slot] = True
+                z[:] = np.nan
+            self._view(slot, inv_off, ldi, n, n)[:, :] = z
+        return self._enqueue(slot, stream, fn, waits)
+
+    def trsm_apply(self, slot, stream, right, eff_upper, h, w, alpha, inv_off, ldi, b_off, ldb,
+                   x_off, ldx, waits=()):
+        self.n_launches += 1
+        n = w if right else h
+        assert x_off != b_off
+
+        def fn():
+            z = self._view(slot, inv_off, ldi, n, n)
+            b = self._view(slot, b_off, ldb, h, w)
+            self._view(slot, x_off, ldx, h, w)[:, :] = alpha * (b @ z if right else z @ b)
         return self._enqueue(slot, stream, fn, waits)
 
     def axpy(self, slot, stream, esz, h, w, beta, src_off, src_ld, dst_off, dst_ld, waits=()):

@@ -90,3 +90,16 @@ def test_sym_and_tri_rows_materialise_operators():
                 e, _ = tiled.tri_of(a, uplo, diag, trans)
                 np.testing.assert_array_equal(sampled.tri_rows(a, uplo, diag, trans, slice(8, 30)),
                                               e[8:30])
+
+
+@pytest.mark.parametrize("kind,kw", CASES[:4] + CASES[9:12])
+def test_compute_block_equals_reference_blocks(kind, kw):
+    a, b, c0, full, alpha, beta, p, t = _setup(kind, kw)
+    m, n = c0.shape
+    blocks = sampled.sample_blocks(kind, m, n, t, 3, seed=2, side=p.get("side", "left"),
+                                   uplo=p.get("uplo", "upper"))
+    views = sampled.block_views(full, blocks, t)
+    for blk in blocks:
+        c0b = sampled.snapshot_blocks(c0, [blk], t)[blk]
+        got = sampled.compute_block(kind, a, b, c0b, blk, tile=t, alpha=alpha, beta=beta, **p)
+        np.testing.assert_allclose(got, views[blk], rtol=1e-13, atol=1e-14)

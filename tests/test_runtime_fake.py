@@ -256,3 +256,47 @@ def test_randomized_routines_fake_engine(case):
     OT.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
     np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-10,
                                atol=1e-10 * max(1.0, float(np.max(np.abs(ref)))))
+
+
+@pytest.mark.parametrize("ndev", [1, 2])
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "trsm"], ids=lambda c: c["name"])
+def test_trsm_inverse_path_matches_reference(case, ndev):
+    """The inverse-based diagonal step (X = alpha inv(E) B, inv(E) computed once per
+    diagonal tile) forced on every tile order, resident arenas: same results as the
+    reference's substitution (every side / uplo / trans / diag variant)."""
+    call = call_of(case)
+    topo_r = Topology([DeviceDesc(i, peer_group="g") for i in range(ndev)])
+    eng = FakeEngine(ndev, seed=len(case["name"]), arena_bytes=1 << 24)
+    res = run_call(call, topo_r, RunOptions(chunk_steps=2, trsm_inverse_min=1), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-10, atol=1e-10)
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+
+
+def test_trsm_inverse_computed_once_per_diagonal_tile():
+    call = build_call("trsm", m=64, n=96, k=64, tile_size=16, seed=3, uplo="lower",
+                      trsm_scaled=True)
+    eng = FakeEngine(1, seed=1, arena_bytes=1 << 24)
+    calls = []
+    orig = eng.trsm_inverse
+
+    def spy(*a, **kw):
+        calls.append(a[7] if len(a) > 7 else None)
+        return orig(*a, **kw)
+    eng.trsm_inverse = spy
+    a = call.a.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    run_call(call, Topology([DeviceDesc(0)]), RunOptions(trsm_inverse_min=1), engine=eng)
+    assert len(calls) == 4                     # 4 diagonal tiles, 6 tile columns each
+    from oracle import tiled
+    ref = c0.copy()
+    tiled.run_tiled("trsm", a, ref, None, tile_size=16, alpha=1.0, uplo="lower")
+    np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-11, atol=1e-11)
+
+
+def test_trsm_inverse_path_raises_singular():
+    call = build_call("trsm", m=48, n=32, k=48, tile_size=16, seed=2, uplo="lower",
+                      trsm_scaled=True)
+    call.a.matrix.as_2d()[20, 20] = 0.0
+    with pytest.raises(SingularMatrixError):
+        run_call(call, Topology([DeviceDesc(0)]), RunOptions(trsm_inverse_min=1),
+                 engine=FakeEngine(1, seed=1, arena_bytes=1 << 24))

@@ -31,6 +31,10 @@ int bx_gemm_task_packed(int d, int s, int f, int ta, int tb, int tr, int h, int 
                         double al, double be, uint64_t c, int lc, int n, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_trsm_tile(int d, int s, int r, int u, int t, int un, int h, int w, double al, uint64_t a, int la,
                  uint64_t b, int lb, int n, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_trsm_inverse(int d, int s, int u, int t, int un, int n, uint64_t a, int la, uint64_t o, int lo,
+                    int nw, const int *wt, int *ev) { launches++; return EV(ev); }
+int bx_trsm_apply(int d, int s, int r, int eu, int h, int w, double al, uint64_t i, int li, uint64_t b, int lb,
+                  uint64_t x, int lx, int nw, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_materialize(int d, int s, int m, int u, int t, int un, int n, uint64_t a, int la, uint64_t o, int lo,
                    int nw, const int *wt, int *ev) { launches++; return EV(ev); }
 int bx_axpy_tile(int d, int s, int e, int h, int w, double be, uint64_t a, int la, uint64_t o, int lo,
