@@ -96,6 +96,14 @@ int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps,
 int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
                         const int64_t* steps, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
                         const int* wait, int* ev_out);
+/* a launch group's tile fetches in one call (resident issue path): n rows of 8 int64
+ * {kind | eb << 8, dst_off, dst_ld, src, src_ld | src_off, h | bytes, w, wait_ev};
+ * kind 0 = 2-d H2D tile (src = pinned host address), 1 = peer copy (src = device slot);
+ * records one event per lane used (ev_h2d / ev_p2p, -1 if unused): in-order lanes, so it
+ * marks every tile of the batch on that lane (replaces per-tile bx_h2d_tile/bx_p2p_tile
+ * calls and events: scheduler.py:248-281 fetch, cache.py:312-322 copy_from_peer) */
+int bx_copy_batch(int dev, int n, const int64_t* ops, int n_wait, const int* wait, int* ev_h2d,
+                  int* ev_p2p);
 /* in-place triangular solve of B (h x w) against the diagonal tile A */
 int bx_trsm_tile(int dev, int stream, int side_right, int upper, int trans, int unit, int h,
                  int w, double alpha, uint64_t a_off, int lda, uint64_t b_off, int ldb, int n_wait,

@@ -46,6 +46,7 @@ _SIGS = {
     "bx_h2d_tile": [_i, _u64, _i, _p, _i64, _i, _i, _i, _i, _pi, _pi],
     "bx_d2h_tile": [_i, _u64, _i, _p, _i64, _i, _i, _i, _i, _pi, _pi],
     "bx_p2p_tile": [_i, _u64, _i, _u64, _u64, _i, _pi, _pi],
+    "bx_copy_batch": [_i, _i, _p, _i, _pi, _pi, _pi],
     "bx_gemm_task": [_i, _i, _i, _i, _i, _i, _i, _i, _pu64, _pi, _pu64, _pi, _pi, _d, _d,
                      _u64, _i, _i, _pi, _pi],
     "bx_sgemm_task": [_i, _i, _i, _i, _i, _i, _i, _pu64, _pi, _pu64, _pi, _pi, C.c_float, C.c_float,

@@ -876,6 +876,56 @@ int bx_p2p_tile(int dst_dev, uint64_t dst_off, int src_dev, uint64_t src_off, ui
   return finish(dst_dev, D->p2p, ev_out);
 }
 
+// A launch group's tile fetches in one call (the runtime's resident issue path): each row
+// {kind | eb << 8, dst_off, dst_ld, src, src_ld | src_off, h | bytes, w, wait_ev} is a
+// 2-d H2D tile copy (kind 0: src = pinned host address, src_ld elements, h x w of eb
+// bytes) or a peer copy (kind 1: src = device slot, src_off, bytes), optionally after a
+// wait event (-1: none; e.g. the source tile's own arrival on the peer).  One event per
+// lane used is recorded after the batch: the lanes are in-order, so that event marks the
+// arrival of every tile the batch put on it.
+int bx_copy_batch(int dev, int n, const int64_t* ops, int n_wait, const int* wait, int* ev_h2d, int* ev_p2p) {
+  Device* D = dev_of(dev);
+  if (!D) return set_err(BX_EINVAL, "bad device");
+  if (n < 0) return set_err(BX_EINVAL, "copy batch: negative count");
+  CUDA_TRY(cudaSetDevice(D->cuda_id));
+  bool used_h2d = false, used_p2p = false;
+  for (int i = 0; i < n; ++i) {
+    const int64_t* r = ops + 8 * i;
+    const int kind = (int)(r[0] & 0xff), eb = (int)(r[0] >> 8);
+    const uint64_t dst_off = (uint64_t)r[1];
+    const int64_t wait_ev = r[7];
+    if (kind == 0) {
+      const int dst_ld = (int)r[2], h = (int)r[5], w = (int)r[6];
+      const int64_t src_ld = r[4];
+      if (h <= 0 || w <= 0 || dst_ld < h || src_ld < h || (eb != 4 && eb != 8) || !r[3])
+        return set_err(BX_EINVAL, "copy batch: bad h2d extents");
+      if (dst_off + (uint64_t)dst_ld * w * eb > D->arena_bytes) return set_err(BX_EINVAL, "copy batch: h2d outside arena");
+      if (!used_h2d && n_wait > 0) { int rc = wait_all(D->h2d, n_wait, wait); if (rc) return rc; }
+      if (wait_ev >= 0) { int we = (int)wait_ev; int rc = wait_all(D->h2d, 1, &we); if (rc) return rc; }
+      CUDA_TRY(cudaMemcpy2DAsync(D->arena + dst_off, (size_t)dst_ld * eb, (const void*)r[3], (size_t)src_ld * eb,
+                                 (size_t)h * eb, w, cudaMemcpyHostToDevice, D->h2d));
+      used_h2d = true;
+    } else if (kind == 1) {
+      Device* S = dev_of((int)r[3]);
+      const uint64_t src_off = (uint64_t)r[4], bytes = (uint64_t)r[5];
+      if (!S) return set_err(BX_EINVAL, "copy batch: bad peer slot");
+      if (dst_off + bytes > D->arena_bytes || src_off + bytes > S->arena_bytes)
+        return set_err(BX_EINVAL, "copy batch: p2p outside arena");
+      if (!used_p2p && n_wait > 0) { int rc = wait_all(D->p2p, n_wait, wait); if (rc) return rc; }
+      if (wait_ev >= 0) { int we = (int)wait_ev; int rc = wait_all(D->p2p, 1, &we); if (rc) return rc; }
+      CUDA_TRY(cudaMemcpyPeerAsync(D->arena + dst_off, D->cuda_id, S->arena + src_off, S->cuda_id, bytes, D->p2p));
+      used_p2p = true;
+    } else {
+      return set_err(BX_EINVAL, "copy batch: unknown op kind");
+    }
+  }
+  if (ev_h2d) *ev_h2d = -1;
+  if (ev_p2p) *ev_p2p = -1;
+  if (used_h2d) { int rc = finish(dev, D->h2d, ev_h2d); if (rc) return rc; }
+  if (used_p2p) { int rc = finish(dev, D->p2p, ev_p2p); if (rc) return rc; }
+  return BX_OK;
+}
+
 int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps, const uint64_t* a_off,
                  const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, double alpha, double beta,
                  uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out) {

@@ -123,6 +123,16 @@ class CudaEngine:
                                      C.byref(ev)), "p2p tile")
         return ev.value
 
+    def copy_batch(self, slot, rows, waits=()):
+        """One launch group's tile fetches (``rows``: array('q'), 8 per copy, see
+        include/blasx_cuda.h bx_copy_batch); returns (H2D lane event, P2P lane event),
+        -1 for a lane the batch did not use."""
+        eh, ep = C.c_int(-1), C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_copy_batch(slot, len(rows) // 8, rows.buffer_info()[0], nw, wp,
+                                       C.byref(eh), C.byref(ep)), "copy batch")
+        return eh.value, ep.value
+
     # ---- one process per GPU (spmd.py) ---------------------------------------------------
 
     def ipc_export(self, slot):

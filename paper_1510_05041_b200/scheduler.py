@@ -30,6 +30,7 @@ from __future__ import annotations
 import os
 import threading
 import time
+from array import array
 from collections import deque
 from dataclasses import dataclass
 from typing import Optional
@@ -221,11 +222,13 @@ class _Active:
     """A task in flight on one compute stream."""
     __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
                  "events", "last_ev", "done_ev", "pending_waits", "flops", "prog", "res",
-                 "next_op", "lazy", "misses", "misses_epoch", "c_pending", "c0_off", "ramp")
+                 "next_op", "lazy", "misses", "misses_epoch", "c_pending", "c0_off", "ramp",
+                 "slot_index")
 
-    def __init__(self, entry, stream):
+    def __init__(self, entry, stream, slot_index=-1):
         self.entry = entry
         self.stream = stream
+        self.slot_index = slot_index
         self.c_off = -1
         self.c_ld = 0
         self.scratch = []        # arena offsets freed at retirement
@@ -288,6 +291,8 @@ class _GpuWorker:
         self._pending_keys = set()   # resident blocks whose arrival event is not known done
         self._inv = {}               # diagonal tile key -> [offset, ld, event, landed]
         self._inv_events = []
+        self._group_events = []      # arrival events shared by a batch of resident blocks
+        self._wb_order = deque()     # issued tasks in write-back order (one in-order D2H lane)
 
     # ---- cache callbacks ------------------------------------------------------------
 
@@ -525,13 +530,13 @@ class _GpuWorker:
         out = {}
         eng = self.eng
         hits = 0
+        misses = [(key, ref) for key, (ref, _m) in keys.items() if key not in blocks]
+        if misses:
+            self._fetch_many(misses)
+            hits -= len(misses)
         for key, (ref, mult) in keys.items():
-            blk = blocks.get(key)
-            if blk is None:
-                blk = self._fetch_resident(key, ref)
-                hits += mult - 1
-            else:
-                hits += mult
+            blk = blocks[key]
+            hits += mult
             wait = None
             ev = blk.ready_ev
             if ev is not None and not blk.ready_done:
@@ -543,6 +548,74 @@ class _GpuWorker:
             out[key] = (blk.offset, blk.ld, wait)
         self.l1_hits += hits
         return out
+
+    def _fetch_many(self, misses) -> None:
+        """Resident-mode misses of one launch group, fetched with ONE engine call
+        (``copy_batch``): per tile the same policy as ``_fetch_resident`` (L2 copy from the
+        lowest-id peer holding the tile, else H2D from pinned host memory), but a single
+        arrival event per copy lane for the whole batch (the lanes are in-order) instead
+        of an engine call and an event per tile."""
+        eng = self.eng
+        if self.trace_on or not hasattr(eng, "copy_batch"):
+            for key, ref in misses:
+                self._fetch_resident(key, ref)
+            return
+        esz = self.esz
+        directory = self.runtime.directory
+        l2 = self.runtime.options.l2_enabled
+        rows = array("q")
+        new_h, new_p = [], []
+        dm = self.dm
+        for key, ref in misses:
+            h, w = ref.phys_height, ref.phys_width
+            ld = device_ld(h)
+            nbytes = ld * w * esz
+            try:
+                off = self.arena.alloc(nbytes)
+            except ArenaOutOfMemoryError:
+                raise CapacityDeadlockError(
+                    f"device {self.device_id}: resident arena exhausted (working-set estimate "
+                    f"too small); set DeviceDesc.arena_capacity to use the evicting cache") from None
+            blk = LruBlock(key, off, nbytes, ld, self.device_id)
+            blk.reader = 1
+            payload = h * w * esz
+            src_id = directory.peer_source(key, self.device_id) if l2 else None
+            src_blk = directory.cache_of(src_id)._blocks.get(key) if src_id is not None else None
+            if src_blk is not None:
+                wait = -1
+                if src_blk.ready_ev is not None and not src_blk.ready_done:
+                    if eng.done(src_blk.ready_ev):
+                        src_blk.ready_done = True
+                    else:
+                        wait = src_blk.ready_ev
+                rows.extend((1, off, ld, eng.slot(src_id), src_blk.offset, nbytes, 0, wait))
+                new_p.append(blk)
+                dm.d2d_in_bytes += payload
+                self.runtime.add_d2d_out(src_id, payload)
+                self.l2_hits += 1
+            else:
+                desc, r0, c0 = self._host_of(ref)
+                rows.extend((esz << 8, off, ld, desc.element_address(r0, c0), desc.leading_dim,
+                             h, w, -1))
+                new_h.append(blk)
+                dm.h2d_bytes += payload
+                self.host_fetches += 1
+        ev_h, ev_p = eng.copy_batch(self.slot, rows)
+        for ev in (ev_h, ev_p):
+            if ev >= 0:
+                self._group_events.append(ev)
+        pend = self._pending_keys
+        blocks = self.cache._blocks
+        with self.cache.lock:
+            for blist, ev in ((new_h, ev_h), (new_p, ev_p)):
+                for blk in blist:
+                    blk.ready_ev = ev          # shared: owned by _group_events
+                    blocks[blk.key] = blk
+                    pend.add(blk.key)
+        for blist in (new_h, new_p):
+            for blk in blist:
+                directory.add_holder(blk.key, self.device_id)
+                self._permanent.append(blk)
 
     def _fetch_resident(self, key, ref):
         """Miss path of resident mode: allocate (never evicts), copy from the lowest-id peer
@@ -628,7 +701,7 @@ class _GpuWorker:
         launches themselves are enqueued by ``_advance`` one launch group at a time."""
         task = entry.task
         opts = self.runtime.options
-        act = _Active(entry, slot_index % self.n_streams)
+        act = _Active(entry, slot_index % self.n_streams, slot_index)
         self._cur = act
         try:
             out = task.out_ref
@@ -788,6 +861,7 @@ class _GpuWorker:
                 h * w * self.esz)
             self.dm.d2h_bytes += h * w * self.esz
             act.events.append(act.done_ev)
+            self._wb_order.append(act)
             if act.lazy:
                 self.l1_hits += task._bx_refs - act.misses
             act.res = None
@@ -825,7 +899,9 @@ class _GpuWorker:
     # ---- completion -----------------------------------------------------------------
 
     def in_flight(self) -> list:
-        return [a.done_ev for a in self.active if a is not None]
+        """The next write-back to complete (the D2H lane is in order, so no later task can
+        complete before it)."""
+        return [self._wb_order[0].done_ev] if self._wb_order else []
 
     def _retire(self, act) -> None:
         task = act.entry.task
@@ -859,14 +935,15 @@ class _GpuWorker:
         self.runtime.complete_task(task)
 
     def _retire_finished(self, block: bool) -> bool:
+        """Retire completed tasks in write-back order: one event query per completed task
+        plus one for the first still in flight, instead of one per active task."""
         got = False
-        for s, act in enumerate(self.active):
-            if act is None or act.done_ev is None:
-                continue
-            if self.eng.done(act.done_ev):
-                self.active[s] = None
-                self._retire(act)
-                got = True
+        q = self._wb_order
+        while q and self.eng.done(q[0].done_ev):
+            act = q.popleft()
+            self.active[act.slot_index] = None
+            self._retire(act)
+            got = True
         return got
 
     def poll(self) -> bool:
@@ -881,6 +958,14 @@ class _GpuWorker:
         for ev in self._inv_events:
             self.eng.release(ev)
         self._inv, self._inv_events = {}, []
+        if self._group_events:
+            shared = set(self._group_events)
+            for blk in self._permanent:
+                if blk.ready_ev in shared:
+                    blk.ready_ev = None
+            for ev in self._group_events:
+                self.eng.release(ev)
+            self._group_events = []
         if self._permanent:
             self.cache.release(self._permanent)
             self._permanent = []

@@ -554,6 +554,11 @@ def _build_runtime_classes():
             return None
 
         # ---- L2 over IPC: first holder fetches from host, the rest copy from it ----
+        def _fetch_many(self, misses):
+            # per tile: each copy publishes its own arrival flag for the other ranks
+            for key, ref in misses:
+                self._fetch_resident(key, ref)
+
         def _fetch_resident(self, key, ref):
             h, w = ref.phys_height, ref.phys_width
             ld = S.device_ld(h)

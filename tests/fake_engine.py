@@ -46,7 +46,7 @@ class FakeEngine:
         self.ops_log = []
         self._lock = threading.RLock()
         for name in ("ensure_arenas", "register_host", "unregister_host", "h2d", "d2h", "p2p",
-                     "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
+                     "copy_batch", "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
                      "sync", "stream_wait", "device_sync"):
             setattr(self, name, _locked(getattr(type(self), name)).__get__(self))
 
@@ -157,6 +157,36 @@ class FakeEngine:
             s = self.arenas[src_slot][src_off // 8:(src_off + nbytes) // 8]
             self.arenas[dst_slot][dst_off // 8:(dst_off + nbytes) // 8] = s
         return self._enqueue(dst_slot, -3, fn, waits)
+
+    def copy_batch(self, slot, rows, waits=()):
+        """bx_copy_batch: each row a 2-d H2D copy from a raw host address or a peer copy;
+        one event per lane used, recorded after the batch."""
+        import ctypes
+        used = {}
+        for i in range(len(rows) // 8):
+            kind, dst_off, dst_ld, src, srcx, hb, w, wait = rows[8 * i:8 * i + 8]
+            eb, kind = kind >> 8, kind & 0xFF
+            wt = list(waits) + ([wait] if wait >= 0 else [])
+            if kind == 0:
+                h = hb
+                dt = np.float64 if eb == 8 else np.float32
+                nbytes = (srcx * (w - 1) + h) * eb
+
+                def fn(src=src, srcx=srcx, h=h, w=w, dst_off=dst_off, dst_ld=dst_ld, eb=eb, dt=dt,
+                       nbytes=nbytes):
+                    raw = np.frombuffer((ctypes.c_char * nbytes).from_address(src), dtype=dt)
+                    full = np.lib.stride_tricks.as_strided(raw, shape=(h, w),
+                                                           strides=(eb, srcx * eb))
+                    self._viewT(slot, dst_off, dst_ld, h, w, eb)[:, :] = full
+                used[-1] = self._enqueue(slot, -1, fn, wt)
+            else:
+                def fn(src=src, srcx=srcx, hb=hb, dst_off=dst_off):
+                    s = self.arenas[src][srcx // 8:(srcx + hb) // 8]
+                    self.arenas[slot][dst_off // 8:(dst_off + hb) // 8] = s
+                used[-3] = self._enqueue(slot, -3, fn, wt)
+        eh = self.record(slot, -1) if -1 in used else -1
+        ep = self.record(slot, -3) if -3 in used else -1
+        return eh, ep
 
     # ---- kernels ----
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
