@@ -91,8 +91,10 @@ int bx_sgemm_task(int dev, int stream, int ta, int tb, int h, int w, int nsteps,
                   const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, float alpha,
                   float beta, uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out);
 /* the same task GEMM (f32 = 0: bx_gemm_task, 1: bx_sgemm_task) with the steps packed as
- * nsteps rows of 5 int64 {a_off, lda, b_off, ldb, depth}: one host array per launch (the
- * runtime's issue path marshals one buffer instead of five) */
+ * nsteps rows of 6 int64 {a_off, lda, b_off, ldb, depth, kmode}: one host array per launch
+ * (the runtime's issue path marshals one buffer instead of five).  kmode (FP64 only;
+ * 0 none, 1/2 A lower/upper, 3/4 B upper/lower triangular) lets each CTA skip the k-range
+ * where that step's triangular operand is zero (TRMM diagonal steps, kernels.py:173-185) */
 int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
                         const int64_t* steps, double alpha, double beta, uint64_t c_off, int ldc, int n_wait,
                         const int* wait, int* ev_out);

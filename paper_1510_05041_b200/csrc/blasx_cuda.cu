@@ -483,7 +483,7 @@ int gemm_tma(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
 
 int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, const double* const* a,
              const int* lda, const double* const* b, const int* ldb, const int* depth, double alpha,
-             double beta, double* c, int ldc, int kmode = bx::KM_NONE) {
+             double beta, double* c, int ldc, const int* kmode = nullptr) {
   if (h < 0 || w < 0 || nsteps < 0) return set_err(BX_EINVAL, "gemm: negative extent");
   if (ldc < (h > 1 ? h : 1)) return set_err(BX_EINVAL, "gemm: ldc < h");
   for (int i = 0; i < nsteps; ++i) {
@@ -509,10 +509,10 @@ int gemm_raw(cudaStream_t s, int ta, int tb, int tri, int h, int w, int nsteps, 
     t.beta = (s0 == 0) ? beta : 1.0;
     int n = nsteps - s0 < bx::G_MAX_STEPS ? nsteps - s0 : bx::G_MAX_STEPS;
     t.nsteps = n;
-    t.kmode = (nsteps == 1) ? kmode : bx::KM_NONE;
     for (int i = 0; i < n; ++i) {
       t.steps[i].a = a[s0 + i]; t.steps[i].b = b[s0 + i];
       t.steps[i].lda = lda[s0 + i]; t.steps[i].ldb = ldb[s0 + i]; t.steps[i].d = depth[s0 + i];
+      t.steps[i].kmode = kmode ? kmode[s0 + i] : bx::KM_NONE;
     }
     int rc = launch_gemm(ta, tb, t, s);
     if (rc) return rc;
@@ -926,9 +926,20 @@ int bx_copy_batch(int dev, int n, const int64_t* ops, int n_wait, const int* wai
   return BX_OK;
 }
 
+static int gemm_task_k(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps, const uint64_t* a_off,
+                       const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, const int* kmode,
+                       double alpha, double beta, uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out);
+
 int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps, const uint64_t* a_off,
                  const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, double alpha, double beta,
                  uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out) {
+  return gemm_task_k(dev, stream, ta, tb, tri, h, w, nsteps, a_off, lda, b_off, ldb, depth, nullptr, alpha, beta,
+                     c_off, ldc, n_wait, wait, ev_out);
+}
+
+static int gemm_task_k(int dev, int stream, int ta, int tb, int tri, int h, int w, int nsteps, const uint64_t* a_off,
+                       const int* lda, const uint64_t* b_off, const int* ldb, const int* depth, const int* kmode,
+                       double alpha, double beta, uint64_t c_off, int ldc, int n_wait, const int* wait, int* ev_out) {
   Device* D = dev_of(dev);
   if (!D) return set_err(BX_EINVAL, "bad device");
   cudaStream_t s = lane_stream(D, stream);
@@ -945,7 +956,8 @@ int bx_gemm_task(int dev, int stream, int ta, int tb, int tri, int h, int w, int
   CUDA_TRY(cudaSetDevice(D->cuda_id));
   int rc = wait_all(s, n_wait, wait);
   if (rc) return rc;
-  rc = gemm_raw(s, ta, tb, tri, h, w, nsteps, ap.data(), lda, bp.data(), ldb, depth, alpha, beta, (double*)(D->arena + c_off), ldc);
+  rc = gemm_raw(s, ta, tb, tri, h, w, nsteps, ap.data(), lda, bp.data(), ldb, depth, alpha, beta, (double*)(D->arena + c_off), ldc,
+                kmode);
   if (rc) return rc;
   return finish(dev, s, ev_out);
 }
@@ -979,18 +991,21 @@ int bx_gemm_task_packed(int dev, int stream, int f32, int ta, int tb, int tri, i
   if (nsteps < 0 || nsteps > 4096) return set_err(BX_EINVAL, "gemm: bad step count");
   std::vector<uint64_t> ao(nsteps > 0 ? nsteps : 1), bo(nsteps > 0 ? nsteps : 1);
   std::vector<int> la(nsteps > 0 ? nsteps : 1), lb(nsteps > 0 ? nsteps : 1), dp(nsteps > 0 ? nsteps : 1);
+  std::vector<int> km(nsteps > 0 ? nsteps : 1);
   for (int i = 0; i < nsteps; ++i) {
-    const int64_t* r = steps + 5 * i;
+    const int64_t* r = steps + 6 * i;
     if (r[0] < 0 || r[2] < 0) return set_err(BX_EINVAL, "gemm: negative operand offset");
+    if (r[5] < bx::KM_NONE || r[5] > bx::KM_B_LOWER) return set_err(BX_EINVAL, "gemm: bad triangular-operand mode");
     ao[i] = (uint64_t)r[0]; la[i] = (int)r[1]; bo[i] = (uint64_t)r[2]; lb[i] = (int)r[3]; dp[i] = (int)r[4];
+    km[i] = (int)r[5];
   }
   if (f32) {
     if (tri) return set_err(BX_EINVAL, "sgemm: no triangle mode");
     return bx_sgemm_task(dev, stream, ta, tb, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(), dp.data(),
                          (float)alpha, (float)beta, c_off, ldc, n_wait, wait, ev_out);
   }
-  return bx_gemm_task(dev, stream, ta, tb, tri, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(), dp.data(),
-                      alpha, beta, c_off, ldc, n_wait, wait, ev_out);
+  return gemm_task_k(dev, stream, ta, tb, tri, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(), dp.data(),
+                     km.data(), alpha, beta, c_off, ldc, n_wait, wait, ev_out);
 }
 
 int bx_sgemm_device(int dev, int stream, int ta, int tb, int m, int n, int k, float alpha, uint64_t a, int lda,
@@ -1072,12 +1087,13 @@ int bx_trsm_apply(int dev, int stream, int side_right, int eff_upper, int h, int
   const double* inv = (const double*)(D->arena + inv_off);
   const double* bp = (const double*)(D->arena + b_off);
   double* x = (double*)(D->arena + x_off);
-  if (!side_right)
-    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &inv, &ldi, &bp, &ldb, &n, alpha, 0.0, x, ldx,
-                  eff_upper ? bx::KM_A_UPPER : bx::KM_A_LOWER);
-  else
-    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &bp, &ldb, &inv, &ldi, &n, alpha, 0.0, x, ldx,
-                  eff_upper ? bx::KM_B_UPPER : bx::KM_B_LOWER);
+  if (!side_right) {
+    const int km = eff_upper ? bx::KM_A_UPPER : bx::KM_A_LOWER;
+    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &inv, &ldi, &bp, &ldb, &n, alpha, 0.0, x, ldx, &km);
+  } else {
+    const int km = eff_upper ? bx::KM_B_UPPER : bx::KM_B_LOWER;
+    rc = gemm_raw(s, 0, 0, 0, h, w, 1, &bp, &ldb, &inv, &ldi, &n, alpha, 0.0, x, ldx, &km);
+  }
   if (rc) return rc;
   return finish(dev, s, ev_out);
 }

@@ -26,20 +26,31 @@ namespace bx {
 constexpr int G_MAX_STEPS = 40;
 
 enum TriMode { TRI_NONE = 0, TRI_LOWER = 1, TRI_UPPER = 2 };
-// Triangular operand (one-step tasks): a CTA reads only the k-range where the triangular
+// Triangular operand (per step): a CTA reads only the k-range where the step's triangular
 // operand can be non-zero — e.g. X = inv(L) B with inv(L) lower: output row block
-// [m0, m0+BM) needs k < m0+BM — halving the flops of a TRSM diagonal-tile apply.
+// [m0, m0+BM) needs k < m0+BM.  Halves the flops of the TRSM diagonal apply and of the
+// TRMM diagonal step (op(tri(A)) B); the operand's other triangle holds exact zeros, so a
+// kernel that ignores the mode computes the same result.
 enum KMode { KM_NONE = 0, KM_A_LOWER = 1, KM_A_UPPER = 2, KM_B_UPPER = 3, KM_B_LOWER = 4 };
+
+__device__ __forceinline__ void step_krange(int d, int kmode, int m0, int n0, int bm, int bn, int& kb, int& ke) {
+  kb = 0;
+  ke = d;
+  if (kmode == KM_A_LOWER) ke = min(d, m0 + bm);
+  else if (kmode == KM_A_UPPER) kb = min(d, m0);
+  else if (kmode == KM_B_UPPER) ke = min(d, n0 + bn);
+  else if (kmode == KM_B_LOWER) kb = min(d, n0);
+}
 
 struct GemmStep {
   const double* a;
   const double* b;
-  int lda, ldb, d, pad_;
+  int lda, ldb, d, kmode;
 };
 
 struct GemmTask {
   double* c;
-  int ldc, h, w, nsteps, tri, group_m, kmode;
+  int ldc, h, w, nsteps, tri, group_m;
   double alpha, beta;
   GemmStep steps[G_MAX_STEPS];
 };
@@ -335,22 +346,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // this CTA's slabs: each step's k-range (restricted for triangular operands; the range
+  // ends are multiples of BM / BN or the step depth, so slabs stay BK-aligned)
   int total = 0;
   bool kfull = true;
   for (int s = 0; s < t.nsteps; ++s) {
-    total += (t.steps[s].d + BK - 1) / BK;
+    int kb, ke;
+    step_krange(t.steps[s].d, t.steps[s].kmode, m0, n0, BM, BN, kb, ke);
+    if (ke > kb) total += (ke - kb + BK - 1) / BK;
     kfull = kfull && (t.steps[s].d % BK == 0);
-  }
-  // triangular operand (one step): this CTA's k-range; kbeg is a multiple of BM or BN
-  int kbeg = 0, kend = -1;
-  if (t.kmode != KM_NONE && t.nsteps == 1) {
-    const int d = t.steps[0].d;
-    kend = d;
-    if (t.kmode == KM_A_LOWER) kend = min(d, m0 + BM);
-    else if (t.kmode == KM_A_UPPER) kbeg = m0;
-    else if (t.kmode == KM_B_UPPER) kend = min(d, n0 + BN);
-    else kbeg = n0;
-    total = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   }
   // Interior CTAs (no tile edge in m, n or any step's k) take an unpredicated cp.async
   // path with no bounds arithmetic; edge CTAs keep the zero-filling path.
@@ -363,7 +367,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   }
   __syncthreads();
 
-  int ld_step = 0, ld_k = kbeg;
+  int ld_step = -1, ld_k = 0, ld_end = 0;
+  auto next_step = [&]() {   // advance the loader to the next step with a non-empty range
+    do {
+      ++ld_step;
+      if (ld_step >= t.nsteps) return;
+      step_krange(t.steps[ld_step].d, t.steps[ld_step].kmode, m0, n0, BM, BN, ld_k, ld_end);
+    } while (ld_end <= ld_k);
+  };
+  next_step();
   auto produce = [&](int slab) {
     const int stage = slab % STAGES;
     if (slab >= STAGES) mbar_wait(&empty[stage], ((slab / STAGES) - 1) & 1);
@@ -380,7 +392,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
       cp_async_arrive_noinc(&full[stage]);
     }
     ld_k += BK;
-    if (ld_k >= (kend >= 0 ? kend : st.d)) { ld_k = 0; ++ld_step; }
+    if (ld_k >= ld_end) next_step();
   };
   for (int s = 0; s < DIST && s < total; ++s) produce(s);
 

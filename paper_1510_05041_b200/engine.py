@@ -174,7 +174,8 @@ class CudaEngine:
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
              f32=False) -> int:
         """One task GEMM launch; ``f32`` selects the tcgen05 TF32 kernel (SGEMM).  ``steps``
-        = [(a_off, lda, b_off, ldb, depth), ...], marshalled as one packed int64 array."""
+        = [(a_off, lda, b_off, ldb, depth, kmode), ...], marshalled as one packed int64
+        array (kmode: triangular operand, program.KM_*)."""
         n = len(steps)
         if f32 and tri:
             raise ValueError("the fp32 task GEMM has no triangle mode")

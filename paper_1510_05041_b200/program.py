@@ -24,10 +24,14 @@ class GemmOp(NamedTuple):
     tri: int             # 0 full, 1 lower, 2 upper
     alpha: float
     beta: float
-    subs: tuple          # ((a_key, b_key, depth), ...)
+    subs: tuple          # ((a_key, b_key, depth, kmode), ...); kmode: triangular operand
+                         # (KM_* below) whose zero half the kernel's CTAs skip
     k: int
     flops: int
     keys: frozenset = frozenset()   # the input tiles the launch reads (scratch excluded)
+
+
+KM_NONE, KM_A_LOWER, KM_A_UPPER, KM_B_UPPER, KM_B_LOWER = 0, 1, 2, 3, 4
 
 
 class MatOp(NamedTuple):
@@ -83,12 +87,12 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
         if cur is not None:
             subs = tuple(cur[5])
             ops.append(GemmOp(cur[0], cur[1], cur[2], cur[3], cur[4], subs, cur[6],
-                              sum(2 * h * w * d for _, _, d in subs),
-                              frozenset(k for ak, bk, _ in subs for k in (ak, bk)
+                              sum(2 * h * w * d for _, _, d, _ in subs),
+                              frozenset(k for ak, bk, _, _ in subs for k in (ak, bk)
                                         if k[0] != "#scratch")))
             cur = None
 
-    def add(ta, tb, tr, alpha, beta, a, b, d, k):
+    def add(ta, tb, tr, alpha, beta, a, b, d, k, km=KM_NONE):
         nonlocal cur
         cap = chunk_steps
         if first_chunk and not any(type(o) is GemmOp for o in ops):
@@ -97,7 +101,7 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
                 or beta != 1.0 or len(cur[5]) >= cap):
             flush()
             cur = [ta, tb, tr, alpha, beta, [], k]
-        cur[5].append((a, b, d))
+        cur[5].append((a, b, d, km))
 
     for st in task.steps:
         kind = st.kind
@@ -120,10 +124,15 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
             scratch.append(n)
             ops.append(MatOp(kind == SYMM_DIAG, st.a.key(), n, idx))
             sk = scratch_key(idx)
+            # op(tri(A)) is triangular (zeros materialised): the kernel skips its zero half
+            eff_upper = (call.uplo == "upper") != call.trans_a
+            tri_op = kind == TRMM_DIAG
             if call.side == "left":
-                add(False, st.b.transposed, 0, st.alpha, st.beta, sk, st.b.key(), n, st.k)
+                km = (KM_A_UPPER if eff_upper else KM_A_LOWER) if tri_op else KM_NONE
+                add(False, st.b.transposed, 0, st.alpha, st.beta, sk, st.b.key(), n, st.k, km)
             else:
-                add(st.b.transposed, False, 0, st.alpha, st.beta, st.b.key(), sk, n, st.k)
+                km = (KM_B_UPPER if eff_upper else KM_B_LOWER) if tri_op else KM_NONE
+                add(st.b.transposed, False, 0, st.alpha, st.beta, st.b.key(), sk, n, st.k, km)
         elif kind == TRSM_SOLVE:
             flush()
             ops.append(TrsmOp(st.a.key(), st.alpha, st.k, st.flops))

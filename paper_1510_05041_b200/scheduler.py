@@ -458,7 +458,7 @@ class _GpuWorker:
         resolved for earlier launches are dropped and re-translated on demand."""
         keys = task_keys(task)
         if type(op) is GemmOp:
-            want = [k for ak, bk, _ in op.subs for k in (ak, bk)]
+            want = [k for ak, bk, _, _ in op.subs for k in (ak, bk)]
         else:
             want = [op.key]
         cache = self.cache
@@ -789,9 +789,9 @@ class _GpuWorker:
                 if type(op) is GemmOp:
                     steps = []
                     waits = []
-                    for ak, bk, d in op.subs:
+                    for ak, bk, d, km in op.subs:
                         a_, b_ = res[ak], res[bk]
-                        steps.append((a_[0], a_[1], b_[0], b_[1], d))
+                        steps.append((a_[0], a_[1], b_[0], b_[1], d, km))
                         if a_[2] is not None:
                             waits.append(a_[2])
                         if b_[2] is not None:

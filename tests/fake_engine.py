@@ -197,10 +197,20 @@ class FakeEngine:
         def fn():
             c = view(slot, c_off, ldc, h, w)
             acc = np.zeros((h, w))
-            for (ao, lda, bo, ldb, d) in steps:
+            for (ao, lda, bo, ldb, d, km) in steps:
                 a = view(slot, ao, lda, d if ta else h, h if ta else d)
                 b = view(slot, bo, ldb, w if tb else d, d if tb else w)
-                acc += (a.T if ta else a) @ (b.T if tb else b)
+                oa, ob = (a.T if ta else a), (b.T if tb else b)
+                # a triangular-operand step: the half the kernel skips must be zero
+                if km == 1:
+                    assert not np.triu(oa, 1).any(), "KM_A_LOWER on a non-lower operand"
+                elif km == 2:
+                    assert not np.tril(oa, -1).any(), "KM_A_UPPER on a non-upper operand"
+                elif km == 3:
+                    assert not np.tril(ob, -1).any(), "KM_B_UPPER on a non-upper operand"
+                elif km == 4:
+                    assert not np.triu(ob, 1).any(), "KM_B_LOWER on a non-lower operand"
+                acc += oa @ ob
             new = alpha * acc if beta == 0.0 else alpha * acc + beta * c
             if tri:
                 m = np.tril(np.ones((h, w), bool)) if tri == 1 else np.triu(np.ones((h, w), bool))
