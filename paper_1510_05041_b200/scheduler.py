@@ -45,7 +45,7 @@ from .errors import (ArenaOutOfMemoryError, CapacityDeadlockError, ConfigError,
 from .memory import Arena
 from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
                        TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
-from .program import AxpyOp, GemmOp, MatOp, compile_task, scratch_key
+from .program import AxpyOp, GemmOp, MatOp, TrsmOp, compile_task, scratch_key
 from .tiling import device_ld
 
 WORKING_SET_TILES = 12   # reference floor (scheduler.py:49-52): 4 tasks x (C + 2 inputs)
@@ -735,6 +735,16 @@ class _GpuWorker:
                 off = self.cache.allocate_under_pressure(ld * n * self.esz, self)
                 act.scratch.append(off)
                 act.res[scratch_key(i)] = (off, ld, None)
+            last = act.prog.ops[-1] if act.prog.ops else None
+            if type(last) is TrsmOp and self.resident and self._inv_wanted(task):
+                # start inv(E) of this task's diagonal tile now, on another stream, so it
+                # overlaps the task's update GEMMs instead of following them
+                out = task.out_ref
+                n = out.phys_width if self.plan.call.side == "right" else out.phys_height
+                if last.key not in self._inv:
+                    act.res.update(self._resolve_resident(task, frozenset((last.key,))))
+                    ao, al, aw = act.res[last.key]
+                    self._trsm_inverse(last.key, ao, al, aw, (act.stream + 1) % self.n_streams, n)
             act.next_op = 0
             act.flops = task.flops
         finally:
@@ -868,6 +878,12 @@ class _GpuWorker:
             return True
         finally:
             self._cur = None
+
+    def _inv_wanted(self, task) -> bool:
+        opts = self.runtime.options
+        out = task.out_ref
+        n = out.phys_width if self.plan.call.side == "right" else out.phys_height
+        return bool(opts.trsm_inverse_min) and not self.f32 and n >= opts.trsm_inverse_min
 
     def _trsm_inverse(self, key, a_off, a_ld, a_wait, stream, n):
         """inv(E) of the diagonal tile ``key`` for the inverse-based TRSM diagonal step

@@ -194,6 +194,27 @@ def test_small_arena_eviction_on_gpu():
     assert res.metrics.host_fetches > 16 + 32       # evictions forced refetches
 
 
+def test_capacity_deadlock_on_gpu_then_recovers():
+    """Failure path on hardware: an arena one tile above the 12-tile floor cannot hold the
+    C / C0 buffers of 8 in-flight tasks -> CapacityDeadlockError after the pressure sync
+    (cache.py:232-250, scheduler.py:636-643); the engine stays usable and the next call
+    (one task in flight) is correct."""
+    from paper_1510_05041_b200 import CapacityDeadlockError
+    tile = 256 * 256 * 8
+    call = build_call("gemm", m=2048, n=2048, k=2048, tile_size=256, seed=12, beta=1.0)
+    with pytest.raises(CapacityDeadlockError):
+        run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * tile)]),
+                 RunOptions(n_streams=4, tasks_per_stream=2))
+    call = build_call("gemm", m=2048, n=2048, k=2048, tile_size=256, seed=12, beta=1.0)
+    a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * tile)]),
+             RunOptions(n_streams=1, tasks_per_stream=1))
+    ref = c0.copy()
+    tiled.run_tiled("gemm", a, ref, b, tile_size=256, alpha=1.0, beta=1.0)
+    assert _ratio("gemm", call.c.matrix.as_2d(), ref, a, b, c0, 1.0, 1.0, 2048) <= tolerance.BOUND
+
+
 def test_concurrent_mode_and_trace():
     call = build_call("syr2k", m=1100, n=1100, k=700, tile_size=256, seed=9, beta=1.0, uplo="lower")
     a, b = call.a.matrix.as_2d().copy(), call.b.matrix.as_2d().copy()

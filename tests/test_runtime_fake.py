@@ -104,15 +104,19 @@ def test_arena_floor_enforced():
                  engine=FakeEngine(1))
 
 
-def test_capacity_deadlock_when_one_task_cannot_fit():
-    call = build_call("gemm", m=16, n=16, k=64, tile_size=8, seed=1)
-    # 13 tiles of capacity: a 4-stream batch with chunk_steps large pins > arena
-    opts = RunOptions(chunk_steps=64, n_streams=4)
-    try:
-        run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * 512)]), opts,
-                 engine=FakeEngine(1))
-    except CapacityDeadlockError:
-        pass
+def test_capacity_deadlock_when_concurrent_tasks_cannot_fit():
+    """An arena one tile above the reference's 12-tile floor cannot hold 8 in-flight tasks'
+    C (and deferred C0) buffers: after the pressure sync the allocation still fails ->
+    CapacityDeadlockError (cache.py:232-250); with one task in flight the same arena works."""
+    call = build_call("gemm", m=64, n=64, k=64, tile_size=8, seed=1, beta=1.0)
+    with pytest.raises(CapacityDeadlockError):
+        run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * 512)]),
+                 RunOptions(n_streams=4, tasks_per_stream=2), engine=FakeEngine(1))
+    call = build_call("gemm", m=64, n=64, k=64, tile_size=8, seed=1, beta=1.0)
+    a, b, c0 = (x.matrix.as_2d().copy() for x in (call.a, call.b, call.c))
+    run_call(call, Topology([DeviceDesc(0, arena_capacity=13 * 512)]),
+             RunOptions(n_streams=1, tasks_per_stream=1), engine=FakeEngine(1))
+    np.testing.assert_allclose(call.c.matrix.as_2d(), a @ b + c0, rtol=1e-12, atol=1e-12)
 
 
 def test_trsm_singular_raises():

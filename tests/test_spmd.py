@@ -82,6 +82,14 @@ def test_spmd_gpu_ranks_share_one_b200(kind, n, k, tile, extra):
 
 
 @pytest.mark.gpu
+def test_spmd_gpu_singular_aborts_both_ranks():
+    """Failure path on hardware: a zero on the triangle's diagonal, 2 ranks on one B200 —
+    the rank whose solve sees it aborts the call and both ranks raise."""
+    outs = spmd.launch(2, SC.run_singular, 1536, 512, False, timeout=900, devices=[0, 0])
+    assert outs == ["SingularMatrixError", "SingularMatrixError"]
+
+
+@pytest.mark.gpu
 def test_spmd_gpu_three_ranks_trsm():
     outs = spmd.launch(3, SC.run_case, "trsm", 2048, 2048, 512, 6, False, timeout=900,
                        devices=[0, 0, 0])
