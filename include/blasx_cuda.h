@@ -140,6 +140,7 @@ int bx_event_sync(int ev);
 int bx_event_wait_any(int n, const int* evs, int* index, int spin_us);
 int bx_event_elapsed(int ev0, int ev1, float* ms);
 int bx_event_release(int ev);
+int bx_event_release_many(int n, const int* evs); /* a retired task's events in one call */
 int bx_stream_wait(int dev, int stream, int ev);
 int bx_device_sync(int dev);
 int bx_launch_count(uint64_t* n); /* kernels launched by this library since load */

@@ -65,6 +65,7 @@ _SIGS = {
     "bx_event_wait_any": [_i, _pi, _pi, _i],
     "bx_event_elapsed": [_i, _i, _pf],
     "bx_event_release": [_i],
+    "bx_event_release_many": [_i, _pi],
     "bx_stream_wait": [_i, _i, _i],
     "bx_device_sync": [_i],
     "bx_launch_count": [_pu64],

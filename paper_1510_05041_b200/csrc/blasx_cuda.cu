@@ -1222,6 +1222,19 @@ int bx_event_release(int ev) {
   return BX_OK;
 }
 
+int bx_event_release_many(int n, const int* evs) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int i = 0; i < n; ++i) {
+    const int ev = evs[i];
+    if (ev < 0) continue;
+    const int d = ev >> kEvShift, idx = ev & ((1 << kEvShift) - 1);
+    if (d >= (int)g_devs.size() || idx >= (int)g_devs[d].events.size()) return set_err(BX_EINVAL, "bad event");
+    Device& D = g_devs[d];
+    (D.timing[idx] ? D.free_timing : D.free_sync).push_back(idx);
+  }
+  return BX_OK;
+}
+
 int bx_stream_wait(int dev, int stream, int ev) {
   Device* D = dev_of(dev);
   if (!D) return set_err(BX_EINVAL, "bad device");

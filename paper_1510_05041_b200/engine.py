@@ -172,7 +172,7 @@ class CudaEngine:
     # ---- kernels ------------------------------------------------------------------------
 
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
-             f32=False) -> int:
+             f32=False, event=True) -> int:
         """One task GEMM launch; ``f32`` selects the tcgen05 TF32 kernel (SGEMM).  ``steps``
         = [(a_off, lda, b_off, ldb, depth, kmode), ...], marshalled as one packed int64
         array (kmode: triangular operand, program.KM_*)."""
@@ -187,8 +187,8 @@ class CudaEngine:
             nw, wp = 0, None
         N.check(self.lib.bx_gemm_task_packed(slot, stream, int(f32), int(ta), int(tb), tri, h, w, n,
                                              flat.buffer_info()[0], float(alpha), float(beta), c_off,
-                                             ldc, nw, wp,
-                                             C.byref(ev)), "sgemm task" if f32 else "gemm task")
+                                             ldc, nw, wp, C.byref(ev) if event else None),
+                "sgemm task" if f32 else "gemm task")
         return ev.value
 
     def trsm(self, slot, stream, right, upper, trans, unit, h, w, alpha, a_off, lda, b_off, ldb,
@@ -218,12 +218,12 @@ class CudaEngine:
         return ev.value
 
     def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
-                    waits=()) -> int:
+                    waits=(), event=True) -> int:
         ev = C.c_int(-1)
         nw, wp = self._waits(waits)
         N.check(self.lib.bx_materialize(slot, stream, int(mode_sym), int(upper), int(trans),
-                                        int(unit), n, a_off, lda, dst_off, ldd, nw, wp, C.byref(ev)),
-                "materialize")
+                                        int(unit), n, a_off, lda, dst_off, ldd, nw, wp,
+                                        C.byref(ev) if event else None), "materialize")
         return ev.value
 
     def axpy(self, slot, stream, esz, h, w, beta, src_off, src_ld, dst_off, dst_ld,
@@ -269,6 +269,12 @@ class CudaEngine:
     def release(self, ev) -> None:
         if ev is not None and ev >= 0:
             self.lib.bx_event_release(ev)
+
+    def release_many(self, evs) -> None:
+        """Return several events to the pool in one call (a task's events at retirement)."""
+        ids = [e for e in evs if e is not None and e >= 0]
+        if ids:
+            N.check(self.lib.bx_event_release_many(len(ids), N.int_array(ids)), "event release")
 
     def stream_wait(self, slot, lane, ev) -> None:
         N.check(self.lib.bx_stream_wait(slot, lane, ev), "stream wait")

@@ -690,8 +690,9 @@ class _GpuWorker:
             return off, ld, ev
 
     def _launched(self, act, ev) -> None:
-        act.events.append(ev)
-        act.last_ev = ev
+        if ev is not None and ev >= 0:
+            act.events.append(ev)
+            act.last_ev = ev
         act.launched_pins.extend(act.pins)
         act.pins = []
         self.dm.kernel_launches += 1
@@ -810,9 +811,13 @@ class _GpuWorker:
                         waits = list(dict.fromkeys(waits))
                     waits += act.pending_waits
                     act.pending_waits = []
-                    ev = self._timed(stream, lambda wt, op=op, steps=steps: eng.gemm(
+                    # only the task's last launch needs an event (its write-back waits on
+                    # it); earlier launches are ordered by the task's stream
+                    last = i == len(ops)
+                    ev = self._timed(stream, lambda wt, op=op, steps=steps, last=last: eng.gemm(
                         slot, stream, op.ta, op.tb, op.tri, h, w, steps, op.alpha, op.beta,
-                        act.c_off, act.c_ld, wt, f32=self.f32), waits, "KERNEL", op.flops, op.k)
+                        act.c_off, act.c_ld, wt, f32=self.f32, event=last), waits, "KERNEL",
+                        op.flops, op.k)
                     self._launched(act, ev)
                     break
                 elif type(op) is MatOp:
@@ -821,8 +826,10 @@ class _GpuWorker:
                     ev = self._timed(stream, lambda wt, op=op, ao=ao, al=al, so=so, sl=sl: eng.materialize(
                         slot, stream, op.sym, call.uplo == "upper",
                         False if op.sym else call.trans_a, (not op.sym) and call.diag == "unit",
-                        op.n, ao, al, so, sl, wt), [aw] if aw is not None else [], "KERNEL", 0, -1)
-                    act.events.append(ev)
+                        op.n, ao, al, so, sl, wt, event=False), [aw] if aw is not None else [],
+                        "KERNEL", 0, -1)
+                    if ev is not None and ev >= 0:
+                        act.events.append(ev)
                 elif type(op) is AxpyOp:
                     desc, r0, c0 = self._host_of(out)
                     c0_ev = self._timed(LANE_H2D, lambda wt: eng.h2d(
@@ -926,8 +933,7 @@ class _GpuWorker:
         act.pins = act.launched_pins = []
         for off in act.scratch:
             self.arena.free(off)
-        for ev in act.events:
-            self.eng.release(ev)
+        self.eng.release_many(act.events)
         key = task.out_ref.key()
         self.runtime.directory.note_write_back(key)
         if self._retain and self.runtime.options.l1_enabled and not self.cache.contains(key):

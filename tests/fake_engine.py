@@ -190,7 +190,7 @@ class FakeEngine:
 
     # ---- kernels ----
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
-             f32=False):
+             f32=False, event=True):
         self.n_launches += 1
         view = self._view32 if f32 else self._view
 
@@ -217,7 +217,8 @@ class FakeEngine:
                 c[m] = new[m]
             else:
                 c[:, :] = new
-        return self._enqueue(slot, stream, fn, waits)
+        ev = self._enqueue(slot, stream, fn, waits)
+        return ev if event else -1
 
     def trsm(self, slot, stream, right, upper, trans, unit, h, w, alpha, a_off, lda, b_off, ldb,
              waits=()):
@@ -271,7 +272,7 @@ class FakeEngine:
         return self._enqueue(slot, stream, fn, waits)
 
     def materialize(self, slot, stream, mode_sym, upper, trans, unit, n, a_off, lda, dst_off, ldd,
-                    waits=()):
+                    waits=(), event=True):
         self.n_launches += 1
 
         def fn():
@@ -282,7 +283,8 @@ class FakeEngine:
             else:
                 m, _ = O.tri_of(a, uplo, "unit" if unit else "non-unit", bool(trans))
             self._view(slot, dst_off, ldd, n, n)[:, :] = m
-        return self._enqueue(slot, stream, fn, waits)
+        ev = self._enqueue(slot, stream, fn, waits)
+        return ev if event else -1
 
     def singular(self, slot, reset=True):
         f = self.flag[slot]
@@ -318,6 +320,9 @@ class FakeEngine:
         return 1.0
 
     def release(self, ev):
+        pass
+
+    def release_many(self, evs):
         pass
 
     def stream_wait(self, slot, lane, ev):

@@ -48,6 +48,7 @@ int bx_event_sync() { return 0; }
 int bx_event_wait_any(int n, const int *evs, int *idx, int spin) { *idx = 0; return 0; }
 int bx_event_elapsed(int a, int b, float *ms) { *ms = 1.0f; return 0; }
 int bx_event_release() { return 0; }
+int bx_event_release_many() { return 0; }
 int bx_stream_wait() { return 0; }
 int bx_device_sync() { return 0; }
 int bx_launch_count(uint64_t *n) { *n = launches; return 0; }
