@@ -737,7 +737,8 @@ class _GpuWorker:
                 act.scratch.append(off)
                 act.res[scratch_key(i)] = (off, ld, None)
             last = act.prog.ops[-1] if act.prog.ops else None
-            if type(last) is TrsmOp and self.resident and self._inv_wanted(task):
+            if (type(last) is TrsmOp and self.resident and self._inv_wanted(task)
+                    and os.environ.get("BX_TRSM_EARLY_INV", "1") != "0"):
                 # start inv(E) of this task's diagonal tile now, on another stream, so it
                 # overlaps the task's update GEMMs instead of following them
                 out = task.out_ref

@@ -46,3 +46,12 @@ for ndev in ndevs:
               f"{best/nt*1e6:6.1f} us/task  H2D {m.total_h2d_bytes()/1e9:.2f} GB "
               f"P2P {m.total_d2d_bytes()/1e9:.2f} GB tasks/dev {sorted(r.tasks_by_device.values())}",
               flush=True)
+if os.environ.get("BX_PROF"):
+    import cProfile
+    import pstats
+    ndev = ndevs[-1]
+    topo = Topology([DeviceDesc(200 + i, cuda_ordinal=0, peer_group="g") for i in range(ndev)])
+    opts = RunOptions(execution=modes[0], sgemm_precise=False)
+    cProfile.run("run_call(call, topo, opts)", "/tmp/host_rate.prof")
+    st = pstats.Stats("/tmp/host_rate.prof")
+    st.sort_stats("tottime").print_stats(30)

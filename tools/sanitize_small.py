@@ -9,6 +9,7 @@ identity + panel/leaf substitution + apply; and the substitution-only path), the
 SGEMM kernels (1-SM, 2-SM cluster, persistent) and the 3xTF32 split, host<->device tile
 copies and the batched copy path.  Each call is checked against numpy so a kernel that a
 sanitizer run disturbed is also caught."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -36,9 +37,22 @@ def tri(a, uplo, trans=False, unit=False):
     return m.T if trans else m
 
 
+def sgemm(lib):
+    for variant in [int(v) for v in os.environ.get("BX_SAN_SGEMM", "0,1,2").split(",") if v]:
+        lib.bx_set_sgemm_variant(variant)
+        for precise in (False, True):
+            call = build_call("gemm", m=600, n=520, k=512, tile_size=256, seed=6, beta=1.0,
+                              dtype=np.float32)
+            check(f"sgemm variant={variant} precise={precise}", call,
+                  RunOptions(chunk_steps=2, sgemm_precise=precise), lambda a, b, c: a @ b + c, 2e-3)
+    lib.bx_set_sgemm_variant(1)
+
+
 def main():
     lib = _native.load()
     o = RunOptions(chunk_steps=2)
+    if os.environ.get("BX_SAN_ONLY_SGEMM"):
+        return sgemm(lib)
     for ta in (False, True):
         for tb in (False, True):
             call = build_call("gemm", m=700, n=600, k=520, tile_size=256, seed=1, alpha=0.5, beta=0.5,
@@ -64,14 +78,7 @@ def main():
               RunOptions(chunk_steps=2, trsm_inverse_min=inv),
               lambda a, b, c, s=side, u=uplo, t=trans: np.linalg.solve(tri(a, u, t), c) if s == "left"
               else np.linalg.solve(tri(a, u, t).T, c.T).T, 1e-10)
-    for variant in (0, 1, 2):
-        lib.bx_set_sgemm_variant(variant)
-        for precise in (False, True):
-            call = build_call("gemm", m=600, n=520, k=512, tile_size=256, seed=6, beta=1.0,
-                              dtype=np.float32)
-            check(f"sgemm variant={variant} precise={precise}", call,
-                  RunOptions(chunk_steps=2, sgemm_precise=precise), lambda a, b, c: a @ b + c, 2e-3)
-    lib.bx_set_sgemm_variant(1)
+    sgemm(lib)
     print("sanitize_small: all kernels ran and matched", flush=True)
 
 
