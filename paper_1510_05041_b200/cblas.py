@@ -1,6 +1,6 @@
 """Python half of the legacy BLAS ABI (``libblasx.so``, ``include/blasx_cblas.h``).
 
-``csrc/blasx_cblas.cpp`` turns every ``cblas_*`` / Fortran ``*_`` call into one call of a
+``csrc/blasx_cblas.c`` turns every ``cblas_*`` / Fortran ``*_`` call into one call of a
 function below with plain integers (CBLAS enum values; Fortran flag characters are mapped to
 the same enums in C), raw host addresses and sizes.  Here the arguments are checked the way
 reference BLAS checks them (xerbla numbering), CblasRowMajor is rewritten

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -41,6 +42,29 @@ int set_err(int code, const std::string& msg) {
 constexpr int kMaxCompute = 16;
 constexpr int kEvShift = 20;
 
+// Per-device event pool.  Lookups (every wait/record/query) are lock-free: events live in
+// fixed chunks published before `count`, so the per-GPU threads of concurrent mode never
+// serialise on a global lock; only creation and release take the pool's own mutex.
+struct EventPool {
+  static constexpr int kChunk = 4096, kChunks = (1 << kEvShift) / kChunk;
+  std::mutex mu;
+  std::atomic<cudaEvent_t*> chunk[kChunks] = {};
+  std::atomic<int> count{0};
+  std::vector<uint8_t> timing;  // guarded by mu
+  std::vector<int> free_sync, free_timing;
+  ~EventPool() {
+    for (auto& c : chunk) delete[] c.load();
+  }
+  bool lookup(int idx, cudaEvent_t* e) const {
+    if (idx < 0 || idx >= count.load(std::memory_order_acquire)) return false;
+    *e = chunk[idx / kChunk].load(std::memory_order_acquire)[idx % kChunk];
+    return true;
+  }
+  void release(int idx) {  // caller holds mu
+    (timing[idx] ? free_timing : free_sync).push_back(idx);
+  }
+};
+
 struct Device {
   int cuda_id = -1;
   int sms = 0;
@@ -51,9 +75,7 @@ struct Device {
   uint64_t arena_bytes = 0;
   int* flag_host = nullptr;  // mapped pinned
   int* flag_dev = nullptr;
-  std::vector<cudaEvent_t> events;  // id -> event
-  std::vector<int> timing;          // whether created with timing
-  std::vector<int> free_sync, free_timing;
+  std::unique_ptr<EventPool> pool;  // id -> event (lock-free lookup)
   std::vector<const void*> attr_set;  // kernels whose smem attribute is set on this device
   bool ready = false;
 };
@@ -76,14 +98,18 @@ cudaStream_t lane_stream(Device* D, int lane) {
 }
 
 int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
+  EventPool& P = *g_devs[d].pool;
   Device* D = &g_devs[d];
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto& fl = timing ? D->free_timing : D->free_sync;
+  std::lock_guard<std::mutex> lk(P.mu);
+  auto& fl = timing ? P.free_timing : P.free_sync;
   int idx;
   if (!fl.empty()) {
     idx = fl.back();
     fl.pop_back();
+    P.lookup(idx, ev);
   } else {
+    idx = P.count.load(std::memory_order_relaxed);
+    if (idx >= (1 << kEvShift)) return set_err(BX_ENOMEM, "event pool exhausted");
     // events belong to the device current at creation: create on this slot's device
     int cur = -1;
     cudaGetDevice(&cur);
@@ -92,12 +118,16 @@ int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
     cudaError_t err = cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
     if (cur != D->cuda_id && cur >= 0) cudaSetDevice(cur);
     if (err != cudaSuccess) return set_err(BX_ECUDA, std::string("cudaEventCreate: ") + cudaGetErrorString(err));
-    idx = (int)D->events.size();
-    if (idx >= (1 << kEvShift)) return set_err(BX_ENOMEM, "event pool exhausted");
-    D->events.push_back(e);
-    D->timing.push_back(timing ? 1 : 0);
+    cudaEvent_t* c = P.chunk[idx / EventPool::kChunk].load(std::memory_order_relaxed);
+    if (!c) {
+      c = new cudaEvent_t[EventPool::kChunk]();
+      P.chunk[idx / EventPool::kChunk].store(c, std::memory_order_release);
+    }
+    c[idx % EventPool::kChunk] = e;
+    P.timing.push_back(timing ? 1 : 0);
+    P.count.store(idx + 1, std::memory_order_release);
+    *ev = e;
   }
-  *ev = D->events[idx];
   *id = (d << kEvShift) | idx;
   return BX_OK;
 }
@@ -105,11 +135,8 @@ int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
 bool ev_lookup(int id, cudaEvent_t* ev, int* d_out = nullptr) {
   if (id < 0) return false;
   int d = id >> kEvShift, idx = id & ((1 << kEvShift) - 1);
-  if (d >= (int)g_devs.size()) return false;
-  Device& D = g_devs[d];
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (idx >= (int)D.events.size()) return false;
-  *ev = D.events[idx];
+  if (d >= (int)g_devs.size() || !g_devs[d].pool) return false;
+  if (!g_devs[d].pool->lookup(idx, ev)) return false;
   if (d_out) *d_out = d;
   return true;
 }
@@ -734,6 +761,7 @@ int bx_init(int ndev, const int* device_ids, const uint64_t* arena_bytes, int n_
     CUDA_TRY(cudaSetDevice(id));
     if (!D.ready) {
       D.cuda_id = id;
+      if (!D.pool) D.pool.reset(new EventPool());
       CUDA_TRY(cudaDeviceGetAttribute(&D.sms, cudaDevAttrMultiProcessorCount, id));
       CUDA_TRY(cudaHostAlloc((void**)&D.flag_host, sizeof(int), cudaHostAllocMapped));
       *D.flag_host = 0;
@@ -776,7 +804,11 @@ int bx_shutdown(void) {
     if (!D.ready) continue;
     cudaSetDevice(D.cuda_id);
     cudaDeviceSynchronize();
-    for (auto e : D.events) cudaEventDestroy(e);
+    if (D.pool) {
+      cudaEvent_t e;
+      for (int i = 0, n = D.pool->count.load(); i < n; ++i)
+        if (D.pool->lookup(i, &e)) cudaEventDestroy(e);
+    }
     for (int s = 0; s < D.ncomp; ++s) cudaStreamDestroy(D.comp[s]);
     cudaStreamDestroy(D.h2d); cudaStreamDestroy(D.d2h); cudaStreamDestroy(D.p2p);
     if (D.arena) cudaFree(D.arena);
@@ -1214,23 +1246,24 @@ int bx_event_elapsed(int ev0, int ev1, float* ms) {
 int bx_event_release(int ev) {
   if (ev < 0) return BX_OK;
   int d = ev >> kEvShift, idx = ev & ((1 << kEvShift) - 1);
-  if (d >= (int)g_devs.size()) return set_err(BX_EINVAL, "bad event");
-  Device& D = g_devs[d];
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (idx >= (int)D.events.size()) return set_err(BX_EINVAL, "bad event");
-  (D.timing[idx] ? D.free_timing : D.free_sync).push_back(idx);
+  if (d >= (int)g_devs.size() || !g_devs[d].pool) return set_err(BX_EINVAL, "bad event");
+  EventPool& P = *g_devs[d].pool;
+  std::lock_guard<std::mutex> lk(P.mu);
+  if (idx >= P.count.load()) return set_err(BX_EINVAL, "bad event");
+  P.release(idx);
   return BX_OK;
 }
 
 int bx_event_release_many(int n, const int* evs) {
-  std::lock_guard<std::mutex> lk(g_mu);
   for (int i = 0; i < n; ++i) {
     const int ev = evs[i];
     if (ev < 0) continue;
     const int d = ev >> kEvShift, idx = ev & ((1 << kEvShift) - 1);
-    if (d >= (int)g_devs.size() || idx >= (int)g_devs[d].events.size()) return set_err(BX_EINVAL, "bad event");
-    Device& D = g_devs[d];
-    (D.timing[idx] ? D.free_timing : D.free_sync).push_back(idx);
+    if (d >= (int)g_devs.size() || !g_devs[d].pool) return set_err(BX_EINVAL, "bad event");
+    EventPool& P = *g_devs[d].pool;
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (idx >= P.count.load()) return set_err(BX_EINVAL, "bad event");
+    P.release(idx);
   }
   return BX_OK;
 }
