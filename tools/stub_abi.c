@@ -5,7 +5,7 @@
 #include <string.h>
 static int ev_next = 0;
 static uint64_t launches = 0;
-#define EV(p) (*(p) = ev_next++, 0)
+#define EV(p) ((p) ? (*(p) = ev_next++) : 0, 0)
 int bx_version(void) { return 1; }
 int bx_device_count(int *n) { *n = 8; return 0; }
 int bx_device_info(int dev, char *name, int len, int *sms, uint64_t *tot, uint64_t *fr) {
