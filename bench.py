@@ -378,10 +378,12 @@ def link_probe(eng, lib, slot, nbytes=256 << 20, reps=4, peers=None, sync_all=No
     [(src_ptr or slot, kind)] for the peer-to-peer figure (CUDA IPC or cudaMemcpyPeer)."""
     from paper_1510_05041_b200.engine import LANE_D2H, LANE_H2D, LANE_P2P
     rows = 8192
-    cols = max(1, nbytes // (rows * 8))
-    nbytes = rows * cols * 8
-    if eng.arena_capacity(slot) < 2 * nbytes:
+    # small calls have small arenas: copy what fits (>= 16 MB still saturates the link)
+    nbytes = min(nbytes, eng.arena_capacity(slot) // 2)
+    cols = nbytes // (rows * 8)
+    if cols < 256:
         return None
+    nbytes = rows * cols * 8
     host = np.empty(rows * cols, dtype=np.float64)
     host[:] = 1.0
     eng.register_host(host)
@@ -455,7 +457,11 @@ def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parit
         per_dev = val["per_device"]
         h2d_max = max(d["h2d"] for d in per_dev.values())
         p2p_max = max(d["d2d_in"] for d in per_dev.values())
+        d2h_max = max(d.get("d2h", 0) for d in per_dev.values())
+        # the host link is full duplex: H2D and D2H overlap, the slower direction bounds
         t_link = h2d_max / (links["h2d_gbs"] * 1e9)
+        if d2h_max and links.get("d2h_gbs"):
+            t_link = max(t_link, d2h_max / (links["d2h_gbs"] * 1e9))
         if p2p_max:
             t_link += p2p_max / (links["p2p_in_gbs"] * 1e9) if links.get("p2p_in_gbs") else float("nan")
     t_meas = val["ms"] / 1e3
@@ -508,7 +514,8 @@ def _metrics_summary(res):
     mt = res.metrics
     return dict(h2d=mt.total_h2d_bytes(), d2h=mt.total_d2h_bytes(), p2p=mt.total_d2d_bytes(),
                 l1=mt.l1_hits, l2=mt.l2_hits, host=mt.host_fetches,
-                per_device={str(d): dict(h2d=v.h2d_bytes, d2d_in=v.d2d_in_bytes, tasks=v.tasks)
+                per_device={str(d): dict(h2d=v.h2d_bytes, d2h=v.d2h_bytes, d2d_in=v.d2d_in_bytes,
+                                          tasks=v.tasks)
                             for d, v in mt.devices.items()})
 
 
