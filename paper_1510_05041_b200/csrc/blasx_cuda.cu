@@ -200,17 +200,24 @@ int launch_gemm_cfg(const bx::GemmTask& t, cudaStream_t s) {
   return BX_OK;
 }
 
-template <class Cfg, bool TA, bool TB>
-int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s) {
-  if (need_attr((const void*)bx::gemm_task_mb_kernel<Cfg, TA, TB>)) {
-    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_mb_kernel<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg::SMEM_BYTES));
+template <class Cfg, bool TA, bool TB, bool KM>
+int launch_gemm_ws_km(const bx::GemmTask& t, cudaStream_t s) {
+  if (need_attr((const void*)bx::gemm_task_mb_kernel<Cfg, TA, TB, KM>)) {
+    CUDA_TRY(cudaFuncSetAttribute(bx::gemm_task_mb_kernel<Cfg, TA, TB, KM>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   }
   int tiles = ((t.h + Cfg::BM - 1) / Cfg::BM) * ((t.w + Cfg::BN - 1) / Cfg::BN);
-  bx::gemm_task_mb_kernel<Cfg, TA, TB><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(t);
+  bx::gemm_task_mb_kernel<Cfg, TA, TB, KM><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(t);
   g_launches++;
   CUDA_TRY(cudaGetLastError());
   return BX_OK;
+}
+
+template <class Cfg, bool TA, bool TB>
+int launch_gemm_ws(const bx::GemmTask& t, cudaStream_t s) {
+  for (int i = 0; i < t.nsteps; ++i)
+    if (t.steps[i].kmode != bx::KM_NONE) return launch_gemm_ws_km<Cfg, TA, TB, true>(t, s);
+  return launch_gemm_ws_km<Cfg, TA, TB, false>(t, s);
 }
 
 template <bool TA, bool TB>

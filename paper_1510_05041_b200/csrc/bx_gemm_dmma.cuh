@@ -319,7 +319,9 @@ __device__ __forceinline__ void fast_slab(double* s, const double* g, int ld, in
   }
 }
 
-template <class Cfg, bool TA, bool TB>
+// KM: some step has a triangular operand (per-step k-ranges); the plain instantiation keeps
+// the simple step walk of the GEMM hot path (the k-range bookkeeping cost 2 % at 16384^3)
+template <class Cfg, bool TA, bool TB, bool KM = false>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_kernel(const __grid_constant__ GemmTask t) {
   extern __shared__ __align__(128) double smem[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES, DIST = Cfg::DIST;
@@ -351,9 +353,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   int total = 0;
   bool kfull = true;
   for (int s = 0; s < t.nsteps; ++s) {
-    int kb, ke;
-    step_krange(t.steps[s].d, t.steps[s].kmode, m0, n0, BM, BN, kb, ke);
-    if (ke > kb) total += (ke - kb + BK - 1) / BK;
+    if constexpr (KM) {
+      int kb, ke;
+      step_krange(t.steps[s].d, t.steps[s].kmode, m0, n0, BM, BN, kb, ke);
+      if (ke > kb) total += (ke - kb + BK - 1) / BK;
+    } else {
+      total += (t.steps[s].d + BK - 1) / BK;
+    }
     kfull = kfull && (t.steps[s].d % BK == 0);
   }
   // Interior CTAs (no tile edge in m, n or any step's k) take an unpredicated cp.async
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   }
   __syncthreads();
 
-  int ld_step = -1, ld_k = 0, ld_end = 0;
+  int ld_step = KM ? -1 : 0, ld_k = 0, ld_end = 0;
   auto next_step = [&]() {   // advance the loader to the next step with a non-empty range
     do {
       ++ld_step;
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
       step_krange(t.steps[ld_step].d, t.steps[ld_step].kmode, m0, n0, BM, BN, ld_k, ld_end);
     } while (ld_end <= ld_k);
   };
-  next_step();
+  if constexpr (KM) next_step();
   auto produce = [&](int slab) {
     const int stage = slab % STAGES;
     if (slab >= STAGES) mbar_wait(&empty[stage], ((slab / STAGES) - 1) & 1);
@@ -392,7 +398,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
       cp_async_arrive_noinc(&full[stage]);
     }
     ld_k += BK;
-    if (ld_k >= ld_end) next_step();
+    if constexpr (KM) {
+      if (ld_k >= ld_end) next_step();
+    } else if (ld_k >= st.d) {
+      ld_k = 0;
+      ++ld_step;
+    }
   };
   for (int s = 0; s < DIST && s < total; ++s) produce(s);
 
