@@ -97,6 +97,13 @@ class RunOptions:
     critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
                                        # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
+    release_on_issue: bool = True      # TRSM (one process, resident arenas): a solved tile
+                                       # is cached and its dependents released once its
+                                       # solve is *enqueued*; their launches wait on the
+                                       # solve's event on the GPU instead of the producer's
+                                       # write-back + a host poll (the write-back still
+                                       # completes the task).  False = the reference's
+                                       # release-after-write-back
     trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
                                        # (resident arenas): X = alpha inv(E) B with inv(E)
                                        # computed once per diagonal tile; 0 = substitution
@@ -188,6 +195,7 @@ class _Runtime:
         self.total = len(plan.tasks)
         self._done = 0
         self._deps = {t.task_id: t.deps_remaining for t in plan.tasks}
+        self._released = set()   # tasks whose dependents were released at issue
         self._lock = threading.Lock()
         self.trace = []
         self.device_metrics = {d.device_id: DeviceMetrics() for d in topology.devices}
@@ -204,6 +212,19 @@ class _Runtime:
     def complete_task(self, task: Task, at_time: float = 0.0) -> None:
         with self._lock:
             self._done += 1
+            if task.task_id in self._released:
+                return
+            for dep in task.dependents:
+                self._deps[dep] -= 1
+                if self._deps[dep] == 0:
+                    self.queue.put((dep, at_time))
+
+    def release_dependents(self, task: Task, at_time: float = 0.0) -> None:
+        """Release-on-issue (RunOptions.release_on_issue): the task's output is cached on
+        its device with the solve's event as arrival event, so dependents may be issued
+        now; ``complete_task`` then only counts the task."""
+        with self._lock:
+            self._released.add(task.task_id)
             for dep in task.dependents:
                 self._deps[dep] -= 1
                 if self._deps[dep] == 0:
@@ -223,7 +244,7 @@ class _Active:
     __slots__ = ("entry", "stream", "c_off", "c_ld", "scratch", "pins", "launched_pins",
                  "events", "last_ev", "done_ev", "pending_waits", "flops", "prog", "res",
                  "next_op", "lazy", "misses", "misses_epoch", "c_pending", "c0_off", "ramp",
-                 "slot_index")
+                 "slot_index", "retained")
 
     def __init__(self, entry, stream, slot_index=-1):
         self.entry = entry
@@ -242,6 +263,7 @@ class _Active:
         self.c_pending = False   # C move-in not yet enqueued
         self.c0_off = -1         # deferred C move-in buffer (program.defer_c)
         self.ramp = False        # part of the start-up batch (extra slot, short launches)
+        self.retained = None     # output block cached at issue (release_on_issue)
 
 
 class _GpuWorker:
@@ -278,6 +300,7 @@ class _GpuWorker:
         self._snap_id = runtime.plan.snapshot_alias
         self._permanent = []
         self._retain = opts.retain_outputs and runtime.plan.call.kind == "trsm"
+        self._early_release = False   # set by run_plan (single process, resident arenas)
         self.resident = False   # set by run_plan when the arena holds the whole working set
         self._sync_epoch = 0
         self._task_misses = 0
@@ -880,12 +903,36 @@ class _GpuWorker:
             self.dm.d2h_bytes += h * w * self.esz
             act.events.append(act.done_ev)
             self._wb_order.append(act)
+            if self._early_release and task.dependents:
+                self._retain_on_issue(act)
             if act.lazy:
                 self.l1_hits += task._bx_refs - act.misses
             act.res = None
             return True
         finally:
             self._cur = None
+
+    def _retain_on_issue(self, act) -> None:
+        """Release-on-issue: cache the task's solved tile now (state M: the device copy is
+        the only up-to-date one until the write-back lands), with the event after the
+        task's last kernel as its arrival event, and release the dependents.  A dependent
+        on this GPU waits on that event on the GPU; one on a peer copies the tile over
+        NVLink after it (the P2P copy waits on the same event).  The tile's value is final
+        — TRSM writes each output tile once — so early readers see exactly what the
+        write-back publishes."""
+        task = act.entry.task
+        key = task.out_ref.key()
+        if act.last_ev is None or act.last_ev < 0 or self.cache.contains(key):
+            return
+        blk = LruBlock(key, act.c_off, act.c_ld * task.out_ref.phys_width * self.esz, act.c_ld,
+                       self.device_id)
+        blk.ready_ev = act.last_ev
+        self.cache.insert_front(blk)
+        self.cache.pin(blk)
+        self._permanent.append(blk)
+        self._pending_keys.add(key)
+        act.retained = blk
+        self.runtime.release_dependents(task)
 
     def _inv_wanted(self, task) -> bool:
         opts = self.runtime.options
@@ -934,10 +981,19 @@ class _GpuWorker:
         act.pins = act.launched_pins = []
         for off in act.scratch:
             self.arena.free(off)
+        kept = act.retained
+        if kept is not None:
+            # cached at issue: the write-back has landed, so the solve has too; its event
+            # id stays allocated until the call ends (a peer may have read it as a wait)
+            kept.ready_done = True
+            self._inv_events.append(kept.ready_ev)
+            act.events = [e for e in act.events if e != kept.ready_ev]
         self.eng.release_many(act.events)
         key = task.out_ref.key()
-        self.runtime.directory.note_write_back(key)
-        if self._retain and self.runtime.options.l1_enabled and not self.cache.contains(key):
+        if kept is not None:
+            pass   # M -> E: the block (and peer copies of its final value) stay cached
+        elif self._retain and self.runtime.options.l1_enabled and not self.cache.contains(key):
+            self.runtime.directory.note_write_back(key)
             # write-back-then-retain: after the D2H the device copy equals
             # the host copy, so the tile moves M -> E instead of M -> I and dependents read
             # it from L1 / over NVLink instead of re-fetching it from the host
@@ -950,6 +1006,7 @@ class _GpuWorker:
                 self.cache.pin(blk)
                 self._permanent.append(blk)
         else:
+            self.runtime.directory.note_write_back(key)
             self.arena.free(act.c_off)
         if self.plan.call.kind == "trsm" and self.eng.singular(self.slot, reset=True):
             raise SingularMatrixError("zero on a non-unit triangular diagonal")
@@ -1183,6 +1240,7 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
     workers = [_GpuWorker(d, rt) for d in devs]
     for w in workers:
         w.resident = resident[w.slot] and options.l1_enabled
+        w._early_release = w.resident and w._retain and options.release_on_issue
         if not w.resident:
             w._ramp_left = 0      # the start-up batch is for resident arenas only
             # an evicting arena must hold every in-flight task's C and one launch's inputs

@@ -304,3 +304,43 @@ def test_trsm_inverse_path_raises_singular():
     with pytest.raises(SingularMatrixError):
         run_call(call, Topology([DeviceDesc(0)]), RunOptions(trsm_inverse_min=1),
                  engine=FakeEngine(1, seed=1, arena_bytes=1 << 24))
+
+
+@pytest.mark.parametrize("release", [True, False])
+@pytest.mark.parametrize("ndev", [1, 3])
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "trsm"], ids=lambda c: c["name"])
+def test_trsm_release_on_issue_matches_reference(case, ndev, release, monkeypatch):
+    """Release-on-issue (resident arenas): a solved tile is cached and its dependents
+    released when its solve is enqueued, their launches (or peers' P2P copies) waiting on
+    the solve's event on the device.  The randomised stream order of the fake engine
+    exposes a missing wait as wrong numbers; both settings give the reference's output."""
+    from paper_1510_05041_b200 import scheduler as S
+    released = []
+    orig = S._Runtime.release_dependents
+
+    def spy(self, task, at_time=0.0):
+        released.append(task.task_id)
+        return orig(self, task, at_time)
+    monkeypatch.setattr(S._Runtime, "release_dependents", spy)
+    call = call_of(case)
+    topo_r = Topology([DeviceDesc(i, peer_group="g") for i in range(ndev)])
+    eng = FakeEngine(ndev, seed=len(case["name"]) + ndev, arena_bytes=1 << 24)
+    res = run_call(call, topo_r, RunOptions(chunk_steps=2, release_on_issue=release,
+                                            trsm_inverse_min=1 if ndev == 1 else 0), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-10, atol=1e-10)
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    with_deps = [t.task_id for t in res.plan.tasks if t.dependents]
+    assert sorted(released) == (sorted(with_deps) if release else [])
+
+
+def test_trsm_release_on_issue_singular_still_raises():
+    """A zero diagonal is still reported (at the producer's retirement) when dependents
+    were released at issue."""
+    a = np.tril(np.random.default_rng(0).uniform(-1, 1, (32, 32))) + 4 * np.eye(32)
+    a[5, 5] = 0.0
+    b = np.random.default_rng(1).uniform(-1, 1, (32, 16))
+    call = RoutineCall("trsm", a=make_tiled(MatrixDesc.from_array("A", a), 8),
+                       b=None, c=make_tiled(MatrixDesc.from_array("C", b), 8), uplo="lower")
+    with pytest.raises(SingularMatrixError):
+        run_call(call, Topology([DeviceDesc(0)]), RunOptions(chunk_steps=2, trsm_inverse_min=0),
+                 engine=FakeEngine(1, seed=2, arena_bytes=1 << 24))
