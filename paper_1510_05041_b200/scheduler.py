@@ -1240,7 +1240,10 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
     workers = [_GpuWorker(d, rt) for d in devs]
     for w in workers:
         w.resident = resident[w.slot] and options.l1_enabled
-        w._early_release = w.resident and w._retain and options.release_on_issue
+        # a dependent on another GPU must get the tile over L2 (the host copy is stale
+        # until the write-back lands): one GPU, or L2 on with every GPU in one peer group
+        w._early_release = (w.resident and w._retain and options.release_on_issue
+                            and (len(devs) == 1 or (options.l2_enabled and w._one_group)))
         if not w.resident:
             w._ramp_left = 0      # the start-up batch is for resident arenas only
             # an evicting arena must hold every in-flight task's C and one launch's inputs

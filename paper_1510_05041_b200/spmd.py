@@ -444,17 +444,28 @@ def _build_runtime_classes():
             self.error = None
             self.d2d_from = [0] * sess.world
             self.worker = None
+            self._released = set()
 
         def done(self) -> bool:
             return int(self.blk.hdr[2]) >= self.total
 
         def complete_task(self, task, at_time: float = 0.0) -> None:
-            self.worker.publish_output(task)
+            if task.task_id not in self._released:
+                self.worker.publish_output(task)
+                self._release(task)
+            atomic_add(self.blk.hdr, 2, 1)
+
+        def release_dependents(self, task, at_time: float = 0.0) -> None:
+            """Release-on-issue across ranks: the producer published its solved tile with
+            a flag its compute stream sets after the solve (SpmdWorker._retain_on_issue)."""
+            self._released.add(task.task_id)
+            self._release(task)
+
+        def _release(self, task) -> None:
             blk = self.blk
             for dep in task.dependents:
                 if atomic_add(blk.deps, dep, -1) == 1:
                     blk.push(dep)
-            atomic_add(blk.hdr, 2, 1)
 
         def add_d2d_out(self, src_rank, nbytes) -> None:
             self.d2d_from[src_rank] += nbytes
@@ -605,6 +616,27 @@ def _build_runtime_classes():
             self._permanent.append(blk)
             return blk
 
+        def _retain_on_issue(self, act) -> None:
+            """Release-on-issue (one process per GPU): cache the solved tile locally (base
+            class), publish its arena offset, and have this task's compute stream set the
+            tile's arrival flag after the solve — other ranks' IPC copies wait for that flag
+            on their GPU (cuStreamWaitValue32), exactly as for a holder's H2D — then
+            release the dependents through the shared counters."""
+            task = act.entry.task
+            key = task.out_ref.key()
+            if (act.last_ev is None or act.last_ev < 0 or self.cache.contains(key)
+                    or key[0] not in self.tbase):
+                return
+            idx = self._kidx(key)
+            W, r = self.W, self.rank
+            cb = self.blk
+            if self.runtime.options.l2_enabled:
+                if atomic_cas(cb.owner, idx, 0, r + 1) != 0:
+                    return                     # cannot happen: outputs are written once
+                cb.offs[idx * W + r] = act.c_off + 1
+                self.eng.write_flag(self.slot, act.stream, self.flags_dptr + 4 * (idx * W + r), 1)
+            super()._retain_on_issue(act)
+
         def publish_output(self, task) -> None:
             """A retained solved TRSM tile (written back, M -> E) becomes a holder copy
             its dependents on other ranks can copy over NVLink."""
@@ -711,6 +743,10 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
     topo = Topology([DeviceDesc(q, peer_group="spmd") for q in range(W)])
     rt = SpmdRuntime(plan, topo, options, engine, sess, blk)
     w = SpmdWorker(topo.devices[r], rt, sess, blk, tbase, bases, flags_dptr)
+    # release-on-issue needs other ranks to read a solved tile over L2 (never from the host
+    # before its write-back)
+    w._early_release = (w._retain and options.l1_enabled and options.release_on_issue
+                        and (W == 1 or options.l2_enabled))
     w.runtime_trace = []
     rt.workers = [w]
     sess.barrier("call start")

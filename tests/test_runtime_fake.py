@@ -344,3 +344,27 @@ def test_trsm_release_on_issue_singular_still_raises():
     with pytest.raises(SingularMatrixError):
         run_call(call, Topology([DeviceDesc(0)]), RunOptions(chunk_steps=2, trsm_inverse_min=0),
                  engine=FakeEngine(1, seed=2, arena_bytes=1 << 24))
+
+
+@pytest.mark.parametrize("split", ["l2_off", "two_groups"])
+def test_trsm_release_on_issue_off_without_shared_l2(split, monkeypatch):
+    """Dependents on another GPU would read a solved tile from the host before its
+    write-back: with L2 off or GPUs in separate peer groups release-on-issue stays off
+    (and the results stay exact)."""
+    from paper_1510_05041_b200 import scheduler as S
+    released = []
+    monkeypatch.setattr(S._Runtime, "release_dependents",
+                        lambda self, task, at_time=0.0: released.append(task.task_id))
+    call = build_call("trsm", m=64, n=96, k=64, tile_size=16, seed=9, uplo="lower",
+                      trsm_scaled=True)
+    a = call.a.matrix.as_2d().copy()
+    c0 = call.c.matrix.as_2d().copy()
+    groups = ["g", "g", "g"] if split == "l2_off" else ["g", "h", "h"]
+    topo_r = Topology([DeviceDesc(i, peer_group=g) for i, g in enumerate(groups)])
+    run_call(call, topo_r, RunOptions(chunk_steps=2, l2_enabled=split != "l2_off"),
+             engine=FakeEngine(3, seed=4, arena_bytes=1 << 24))
+    assert released == []
+    from oracle import tiled
+    ref = c0.copy()
+    tiled.run_tiled("trsm", a, ref, None, tile_size=16, alpha=1.0, uplo="lower")
+    np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-11, atol=1e-11)
