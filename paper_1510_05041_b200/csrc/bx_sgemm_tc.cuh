@@ -407,6 +407,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           }
         }
       }
+      // producer tail: wait for the leader's last multicast commits on this CTA's "empty"
+      // barriers, so no arrival can land in this SM's shared memory after the CTA exits
+      // (the next CTA scheduled on the SM would see it on its own barriers)
+      for (int it = total > P_STAGES ? total - P_STAGES : 0; it < total; ++it)
+        p_mbar_wait(&empty[it % P_STAGES], (it / P_STAGES) & 1);
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {

@@ -1,5 +1,6 @@
 """Timeline analysis of one host-resident call (record_trace=True): where does e2e time go?
-python tools/trace_e2e.py [n] [tile] [chunk] [tasks_per_stream]"""
+python tools/trace_e2e.py [n] [tile] [chunk] [tasks_per_stream] [first_chunk]
+(BX_KIND=gemm|syrk|syr2k|trsm|trmm, BX_F32=1 for SGEMM)"""
 import sys
 import time
 
@@ -18,7 +19,7 @@ import os
 kind = os.environ.get("BX_KIND", "gemm")
 call = build_call(kind, m=n, n=n, k=n, tile_size=t, seed=0, alpha=1.0,
                   beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0, uplo="lower",
-                  trsm_scaled=True)
+                  trsm_scaled=True, **({"dtype": np.float32} if os.environ.get("BX_F32") else {}))
 eng = get_engine([0])
 for x in [y for y in (call.a, call.b, call.c) if y is not None]:
     eng.register_host(x.matrix.storage)
