@@ -210,6 +210,32 @@ int bx_write_flag(int dev, int lane, uint64_t flag_dptr, uint32_t value, int n_w
 int bx_atomic_add(int64_t* p, int64_t v, int64_t* old);
 int bx_atomic_cas(int64_t* p, int64_t expected, int64_t desired, int64_t* old);
 
+/* ---- resident issue engine (one routine call; replaces the per-tile translate/fetch of
+ * scheduler.py:426-461 + cache.py:97-113 and the per-launch kernel dispatch of
+ * routines.py:456-479 for resident arenas, in one C call per launch) ----
+ * tiles: ntiles rows of 6 int64 {host address, host ld (elements), h, w, element bytes,
+ * device ld}; each GPU d (engine slot slots[d], peer group groups[d]) places tiles in its
+ * arena region [region_off[d], +region_bytes[d]).  A missing tile is copied from the
+ * lowest-id GPU of the same group that holds it (l2 != 0; the copy waits on the holder's
+ * arrival event) or from the host; copies of one call share one arrival event per lane. */
+int bx_ic_create(int ndev, const int* slots, const int* groups, int ntiles, const int64_t* tiles,
+                 const uint64_t* region_off, const uint64_t* region_bytes, int l2, int* id);
+/* releases the call's arrival events (the caller drains its GPUs first) */
+int bx_ic_destroy(int id);
+/* the tile table, valid until bx_ic_destroy: off[d*ntiles+t] (-1 = absent), ev[d*ntiles+t]
+ * (pending arrival event, -1 = landed), holders[t] (bit d), metrics[d*8+k] (k: H2D bytes,
+ * d2d-in bytes, host fetches, L2 hits, d2d-out bytes, tile references served) */
+int bx_ic_state(int id, int64_t** off, int32_t** ev, uint32_t** holders, int64_t** metrics);
+/* make tiles present on GPU d; their offsets / device lds and the distinct arrival
+ * events (<= wait_cap) a consumer must wait on */
+int bx_ic_resolve(int id, int d, int n, const int32_t* tids, int64_t* off_out, int32_t* ld_out, int* n_wait,
+                  int* wait_out, int wait_cap);
+/* bx_gemm_task_packed with tile-id operands: nsteps rows of 4 int32 {a, b, depth, kmode};
+ * an id < 0 names raw[2*(-id-1)..] = (arena offset, ld) (scratch tiles) */
+int bx_ic_gemm(int id, int d, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
+               const int32_t* steps, const int64_t* raw, int nraw, double alpha, double beta, uint64_t c_off,
+               int ldc, int n_wait, const int* wait, int* ev_out);
+
 #ifdef __cplusplus
 }
 #endif

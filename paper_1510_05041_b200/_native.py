@@ -47,6 +47,12 @@ _SIGS = {
     "bx_d2h_tile": [_i, _u64, _i, _p, _i64, _i, _i, _i, _i, _pi, _pi],
     "bx_p2p_tile": [_i, _u64, _i, _u64, _u64, _i, _pi, _pi],
     "bx_copy_batch": [_i, _i, _p, _i, _pi, _pi, _pi],
+    "bx_ic_create": [_i, _pi, _pi, _i, _p, _pu64, _pu64, _i, _pi],
+    "bx_ic_destroy": [_i],
+    "bx_ic_state": [_i, _p, _p, _p, _p],
+    "bx_ic_resolve": [_i, _i, _i, _p, _p, _p, _pi, _pi, _i],
+    "bx_ic_gemm": [_i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _p, _p, _i, _d, _d, _u64, _i, _i, _pi,
+                   _pi],
     "bx_gemm_task": [_i, _i, _i, _i, _i, _i, _i, _i, _pu64, _pi, _pu64, _pi, _pi, _d, _d,
                      _u64, _i, _i, _pi, _pi],
     "bx_sgemm_task": [_i, _i, _i, _i, _i, _i, _i, _pu64, _pi, _pu64, _pi, _pi, C.c_float, C.c_float,

@@ -4,6 +4,7 @@
 // each entry point replaces in the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -1552,6 +1553,256 @@ int bx_atomic_cas(int64_t* p, int64_t expected, int64_t desired, int64_t* old) {
   __atomic_compare_exchange_n(p, &e, desired, false, __ATOMIC_SEQ_CST, __ATOMIC_SEQ_CST);
   *old = e;
   return BX_OK;
+}
+
+// ---- resident issue engine ------------------------------------------------------------
+// One routine call's input tiles in a per-GPU region of each arena (resident arenas hold
+// every input tile, so nothing is ever evicted).  The Python runtime keeps the scheduling
+// policy (stations, Eq. 3, stealing) and hands a launch's operands over as tile ids; the
+// translation (L1 hit / L2 copy from the lowest-id peer holding the tile / H2D from the
+// pinned host operand, the reference's policy, scheduler.py:426-461 + cache.py:97-113),
+// the copies and the launch are one C call.  The tile table (offsets, arrival events,
+// holder masks) is exported to Python as plain arrays for Eq. 3 and the metrics.
+
+struct IcTile {
+  uint64_t host;
+  int64_t host_ld;
+  int h, w, esz, ld;
+  uint64_t bytes;
+};
+
+struct IcCall {
+  int ndev = 0, ntiles = 0, l2 = 1;
+  std::vector<int> slot, group;
+  std::vector<IcTile> tiles;
+  std::vector<int64_t> off;       // [d * ntiles + t]: arena offset, -1 = not on GPU d
+  std::vector<int32_t> ev;        // arrival event (shared by a copy batch), -1 = landed
+  std::vector<uint32_t> holders;  // [t]: bit d set once GPU d holds (or is fetching) t
+  std::vector<uint64_t> cur, end; // per-GPU bump allocator inside its region
+  std::vector<int64_t> met;       // [d * 8 + k]: h2d bytes, d2d-in bytes, host fetches,
+                                  // L2 hits, d2d-out bytes, tile references served
+  std::vector<int> owned;         // arrival events, released by bx_ic_destroy
+  std::vector<uint32_t> stamp;    // per-tile dedupe marks for one resolve
+  uint32_t epoch = 0;
+  std::mutex mu;
+};
+
+std::mutex g_ic_mu;
+std::vector<std::unique_ptr<IcCall>> g_ic;
+
+IcCall* ic_of(int id) {
+  std::lock_guard<std::mutex> lk(g_ic_mu);
+  if (id < 0 || id >= (int)g_ic.size()) return nullptr;
+  return g_ic[id].get();
+}
+
+// Make every tile of `tids` present on GPU d (caller holds C.mu): missing tiles are
+// allocated in d's region and fetched — over L2 from the lowest-id peer of d's group that
+// holds the tile (the copy waits on that holder's arrival event), else from the host —
+// with one arrival event per copy lane for the whole batch.  Appends the distinct
+// arrival events the caller's launch must wait on to `waits`.
+int ic_resolve(IcCall& C, int d, int n, const int32_t* tids, std::vector<int>& waits) {
+  Device* D = dev_of(C.slot[d]);
+  if (!D) return set_err(BX_EINVAL, "ic: bad device");
+  const int nt = C.ntiles;
+  if (++C.epoch == 0) { std::fill(C.stamp.begin(), C.stamp.end(), 0u); C.epoch = 1; }
+  std::vector<int> new_h, new_p;
+  bool set_dev = false;
+  for (int i = 0; i < n; ++i) {
+    const int t = tids[i];
+    if (t < 0 || t >= nt) return set_err(BX_EINVAL, "ic: tile id out of range");
+    if (C.stamp[t] == C.epoch) continue;
+    C.stamp[t] = C.epoch;
+    const size_t idx = (size_t)d * nt + t;
+    int64_t* m = &C.met[(size_t)d * 8];
+    if (C.off[idx] >= 0) {
+      const int e = C.ev[idx];
+      if (e >= 0) {
+        cudaEvent_t ce;
+        if (ev_lookup(e, &ce) && cudaEventQuery(ce) == cudaSuccess) C.ev[idx] = -1;
+        else if (std::find(waits.begin(), waits.end(), e) == waits.end()) waits.push_back(e);
+      }
+      continue;
+    }
+    const IcTile& T = C.tiles[t];
+    const uint64_t o = (C.cur[d] + 255) & ~(uint64_t)255;
+    if (o + T.bytes > C.end[d]) return set_err(BX_ENOMEM, "ic: resident region exhausted");
+    C.cur[d] = o + T.bytes;
+    C.off[idx] = (int64_t)o;
+    if (!set_dev) { CUDA_TRY(cudaSetDevice(D->cuda_id)); set_dev = true; }
+    int src = -1;
+    if (C.l2) {
+      const uint32_t h = C.holders[t];
+      for (int e = 0; e < C.ndev; ++e)
+        if (e != d && ((h >> e) & 1u) && C.group[e] == C.group[d]) { src = e; break; }
+    }
+    const uint64_t payload = (uint64_t)T.h * T.w * T.esz;
+    if (src >= 0) {
+      const size_t sidx = (size_t)src * nt + t;
+      Device* S = dev_of(C.slot[src]);
+      if (!S) return set_err(BX_EINVAL, "ic: bad peer device");
+      if (C.ev[sidx] >= 0) { int we = C.ev[sidx]; int rc = wait_all(D->p2p, 1, &we); if (rc) return rc; }
+      CUDA_TRY(cudaMemcpyPeerAsync(D->arena + o, D->cuda_id, S->arena + C.off[sidx], S->cuda_id, T.bytes, D->p2p));
+      new_p.push_back(t);
+      m[1] += (int64_t)payload;
+      m[3] += 1;
+      C.met[(size_t)src * 8 + 4] += (int64_t)payload;
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(D->arena + o, (size_t)T.ld * T.esz, (const void*)T.host,
+                                 (size_t)T.host_ld * T.esz, (size_t)T.h * T.esz, T.w,
+                                 cudaMemcpyHostToDevice, D->h2d));
+      new_h.push_back(t);
+      m[0] += (int64_t)payload;
+      m[2] += 1;
+    }
+    C.holders[t] |= 1u << d;
+  }
+  for (int lane = 0; lane < 2; ++lane) {
+    std::vector<int>& lst = lane == 0 ? new_h : new_p;
+    if (lst.empty()) continue;
+    int e = -1;
+    int rc = finish(C.slot[d], lane == 0 ? D->h2d : D->p2p, &e);
+    if (rc) return rc;
+    C.owned.push_back(e);
+    for (int t : lst) C.ev[(size_t)d * nt + t] = e;
+    waits.push_back(e);
+  }
+  return BX_OK;
+}
+
+int bx_ic_create(int ndev, const int* slots, const int* groups, int ntiles, const int64_t* tiles,
+                 const uint64_t* region_off, const uint64_t* region_bytes, int l2, int* id) {
+  if (ndev <= 0 || ndev > 32 || ntiles < 0) return set_err(BX_EINVAL, "ic: bad sizes");
+  std::unique_ptr<IcCall> C(new IcCall());
+  C->ndev = ndev;
+  C->ntiles = ntiles;
+  C->l2 = l2;
+  C->slot.assign(slots, slots + ndev);
+  C->group.assign(groups, groups + ndev);
+  C->tiles.resize(ntiles);
+  for (int t = 0; t < ntiles; ++t) {
+    const int64_t* r = tiles + 6 * t;   // host address, host ld, h, w, element bytes, device ld
+    IcTile& T = C->tiles[t];
+    T.host = (uint64_t)r[0]; T.host_ld = r[1]; T.h = (int)r[2]; T.w = (int)r[3]; T.esz = (int)r[4];
+    T.ld = (int)r[5];
+    if (!T.host || T.h <= 0 || T.w <= 0 || T.ld < T.h || T.host_ld < T.h || (T.esz != 4 && T.esz != 8))
+      return set_err(BX_EINVAL, "ic: bad tile descriptor " + std::to_string(t));
+    T.bytes = (uint64_t)T.ld * T.w * T.esz;
+  }
+  for (int d = 0; d < ndev; ++d) {
+    Device* D = dev_of(slots[d]);
+    if (!D) return set_err(BX_EINVAL, "ic: bad device slot");
+    if (region_off[d] + region_bytes[d] > D->arena_bytes) return set_err(BX_EINVAL, "ic: region outside arena");
+  }
+  C->off.assign((size_t)ndev * ntiles, -1);
+  C->ev.assign((size_t)ndev * ntiles, -1);
+  C->holders.assign(ntiles, 0u);
+  C->cur.assign(region_off, region_off + ndev);
+  C->end.resize(ndev);
+  for (int d = 0; d < ndev; ++d) C->end[d] = region_off[d] + region_bytes[d];
+  C->met.assign((size_t)ndev * 8, 0);
+  C->stamp.assign(ntiles, 0u);
+  std::lock_guard<std::mutex> lk(g_ic_mu);
+  for (int i = 0; i < (int)g_ic.size(); ++i)
+    if (!g_ic[i]) { g_ic[i] = std::move(C); *id = i; return BX_OK; }
+  g_ic.push_back(std::move(C));
+  *id = (int)g_ic.size() - 1;
+  return BX_OK;
+}
+
+int bx_ic_destroy(int id) {
+  std::unique_ptr<IcCall> C;
+  {
+    std::lock_guard<std::mutex> lk(g_ic_mu);
+    if (id < 0 || id >= (int)g_ic.size() || !g_ic[id]) return set_err(BX_EINVAL, "ic: bad id");
+    C = std::move(g_ic[id]);
+  }
+  if (!C->owned.empty()) return bx_event_release_many((int)C->owned.size(), C->owned.data());
+  return BX_OK;
+}
+
+int bx_ic_state(int id, int64_t** off, int32_t** ev, uint32_t** holders, int64_t** metrics) {
+  IcCall* C = ic_of(id);
+  if (!C) return set_err(BX_EINVAL, "ic: bad id");
+  *off = C->off.data();
+  *ev = C->ev.data();
+  *holders = C->holders.data();
+  *metrics = C->met.data();
+  return BX_OK;
+}
+
+int bx_ic_resolve(int id, int d, int n, const int32_t* tids, int64_t* off_out, int32_t* ld_out, int* n_wait,
+                  int* wait_out, int wait_cap) {
+  IcCall* C = ic_of(id);
+  if (!C || d < 0 || d >= C->ndev) return set_err(BX_EINVAL, "ic: bad id/device");
+  std::lock_guard<std::mutex> lk(C->mu);
+  std::vector<int> waits;
+  int rc = ic_resolve(*C, d, n, tids, waits);
+  if (rc) return rc;
+  if ((int)waits.size() > wait_cap) return set_err(BX_EINVAL, "ic: wait buffer too small");
+  for (int i = 0; i < n; ++i) {
+    off_out[i] = C->off[(size_t)d * C->ntiles + tids[i]];
+    ld_out[i] = C->tiles[tids[i]].ld;
+  }
+  for (size_t i = 0; i < waits.size(); ++i) wait_out[i] = waits[i];
+  *n_wait = (int)waits.size();
+  C->met[(size_t)d * 8 + 5] += n;
+  return BX_OK;
+}
+
+// One task GEMM launch whose operands are tile ids: steps = nsteps rows of
+// {a, b, depth, kmode}; an operand id < 0 names raw[-id - 1] = (arena offset, ld) (scratch
+// tiles).  The launch waits on `wait` plus the arrival events of its tiles.
+int bx_ic_gemm(int id, int d, int stream, int f32, int ta, int tb, int tri, int h, int w, int nsteps,
+               const int32_t* steps, const int64_t* raw, int nraw, double alpha, double beta, uint64_t c_off,
+               int ldc, int n_wait, const int* wait, int* ev_out) {
+  IcCall* C = ic_of(id);
+  if (!C || d < 0 || d >= C->ndev) return set_err(BX_EINVAL, "ic: bad id/device");
+  if (nsteps < 0 || nsteps > 4096) return set_err(BX_EINVAL, "ic gemm: bad step count");
+  std::vector<int> waits(wait, wait + n_wait);
+  std::vector<int32_t> tids;
+  tids.reserve(2 * nsteps);
+  for (int i = 0; i < 2 * nsteps; ++i) {
+    const int32_t v = steps[4 * (i / 2) + (i & 1)];
+    if (v >= 0) tids.push_back(v);
+    else if (-v - 1 >= nraw) return set_err(BX_EINVAL, "ic gemm: raw operand out of range");
+  }
+  std::vector<uint64_t> ao(nsteps > 0 ? nsteps : 1), bo(nsteps > 0 ? nsteps : 1);
+  std::vector<int> la(nsteps > 0 ? nsteps : 1), lb(nsteps > 0 ? nsteps : 1), dp(nsteps > 0 ? nsteps : 1),
+      km(nsteps > 0 ? nsteps : 1);
+  {
+    std::lock_guard<std::mutex> lk(C->mu);
+    int rc = ic_resolve(*C, d, (int)tids.size(), tids.data(), waits);
+    if (rc) return rc;
+    C->met[(size_t)d * 8 + 5] += (int64_t)tids.size();
+    const int nt = C->ntiles;
+    for (int i = 0; i < nsteps; ++i) {
+      const int32_t* r = steps + 4 * i;
+      for (int o = 0; o < 2; ++o) {
+        uint64_t off;
+        int ld;
+        if (r[o] >= 0) {
+          off = (uint64_t)C->off[(size_t)d * nt + r[o]];
+          ld = C->tiles[r[o]].ld;
+        } else {
+          off = (uint64_t)raw[2 * (-r[o] - 1)];
+          ld = (int)raw[2 * (-r[o] - 1) + 1];
+        }
+        (o ? bo : ao)[i] = off;
+        (o ? lb : la)[i] = ld;
+      }
+      dp[i] = r[2];
+      km[i] = r[3];
+      if (km[i] < bx::KM_NONE || km[i] > bx::KM_B_LOWER) return set_err(BX_EINVAL, "ic gemm: bad kmode");
+    }
+  }
+  if (f32) {
+    if (tri) return set_err(BX_EINVAL, "sgemm: no triangle mode");
+    return bx_sgemm_task(C->slot[d], stream, ta, tb, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(),
+                         dp.data(), (float)alpha, (float)beta, c_off, ldc, (int)waits.size(), waits.data(), ev_out);
+  }
+  return gemm_task_k(C->slot[d], stream, ta, tb, tri, h, w, nsteps, ao.data(), la.data(), bo.data(), lb.data(),
+                     dp.data(), km.data(), alpha, beta, c_off, ldc, (int)waits.size(), waits.data(), ev_out);
 }
 
 }  // extern "C"

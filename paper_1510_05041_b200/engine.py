@@ -133,6 +133,45 @@ class CudaEngine:
                                        C.byref(eh), C.byref(ep)), "copy batch")
         return eh.value, ep.value
 
+    # ---- resident issue engine (one routine call) ------------------------------------------
+
+    def ic_create(self, slots, groups, tiles, region_off, region_bytes, l2) -> "IcTable":
+        """The call's tile table (``tiles``: array('q'), 6 per tile, see bx_ic_create)."""
+        tid = C.c_int(-1)
+        N.check(self.lib.bx_ic_create(len(slots), N.int_array(slots), N.int_array(groups),
+                                      len(tiles) // 6, tiles.buffer_info()[0],
+                                      N.u64_array(region_off), N.u64_array(region_bytes),
+                                      int(l2), C.byref(tid)), "ic create")
+        return IcTable(self, tid.value, len(slots), len(tiles) // 6)
+
+    def ic_destroy(self, table) -> None:
+        N.check(self.lib.bx_ic_destroy(table.id), "ic destroy")
+
+    def ic_resolve(self, table, d, tids):
+        """Offsets, device lds and pending arrival events of ``tids`` (array('i')) on GPU
+        ``d`` of the table, fetching the missing ones."""
+        n = len(tids)
+        offs, lds = (C.c_int64 * max(1, n))(), (C.c_int32 * max(1, n))()
+        cap = 2 * n + 2
+        waits, nw = (C.c_int * cap)(), C.c_int(0)
+        N.check(self.lib.bx_ic_resolve(table.id, d, n, tids.buffer_info()[0], offs, lds,
+                                       C.byref(nw), waits, cap), "ic resolve")
+        return list(offs[:n]), list(lds[:n]), list(waits[:nw.value])
+
+    def ic_gemm(self, table, d, stream, f32, ta, tb, tri, h, w, steps, raw, alpha, beta, c_off,
+                ldc, waits=(), event=True) -> int:
+        """One task GEMM launch over tile ids (``steps``: array('i'), 4 per step; ``raw``:
+        array('q') of (offset, ld) for negative ids, or None)."""
+        ev = C.c_int(-1)
+        nw, wp = self._waits(waits)
+        N.check(self.lib.bx_ic_gemm(table.id, d, stream, int(f32), int(ta), int(tb), tri, h, w,
+                                    len(steps) // 4, steps.buffer_info()[0],
+                                    raw.buffer_info()[0] if raw else None,
+                                    len(raw) // 2 if raw else 0, float(alpha), float(beta), c_off,
+                                    ldc, nw, wp, C.byref(ev) if event else None),
+                "ic gemm")
+        return ev.value
+
     # ---- one process per GPU (spmd.py) ---------------------------------------------------
 
     def ipc_export(self, slot):
@@ -286,6 +325,26 @@ class CudaEngine:
         n = C.c_uint64(0)
         self.lib.bx_launch_count(C.byref(n))
         return n.value
+
+
+class IcTable:
+    """A call's resident tile table in the engine, with numpy views of its state arrays
+    (offsets, pending arrival events, holder masks, per-GPU counters) for Eq. 3 and the
+    metrics."""
+
+    def __init__(self, eng, tid, ndev, ntiles):
+        import numpy as np
+        self.id, self.ndev, self.ntiles = tid, ndev, ntiles
+        ptrs = [C.c_void_p() for _ in range(4)]
+        N.check(eng.lib.bx_ic_state(tid, *[C.byref(p) for p in ptrs]), "ic state")
+        n = max(1, ndev * ntiles)
+
+        def view(p, ctype, count):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ctype)), shape=(count,))
+        self.off = view(ptrs[0], C.c_int64, n)[:ndev * ntiles].reshape(ndev, ntiles)
+        self.ev = view(ptrs[1], C.c_int32, n)[:ndev * ntiles].reshape(ndev, ntiles)
+        self.holders = view(ptrs[2], C.c_uint32, max(1, ntiles))[:ntiles]
+        self.metrics = view(ptrs[3], C.c_int64, ndev * 8).reshape(ndev, 8)
 
 
 _ENGINE = None

@@ -301,6 +301,11 @@ class _GpuWorker:
         self._permanent = []
         self._retain = opts.retain_outputs and runtime.plan.call.kind == "trsm"
         self._early_release = False   # set by run_plan (single process, resident arenas)
+        self.ic = None                # resident issue engine table (engine.IcTable), if used
+        self.ic_d = -1                # this GPU's index in it
+        self._ic_region = -1
+        self._ic_group = 0            # bit mask of the GPUs in this GPU's peer group
+        self._ic_refs = 0             # step references of the tasks issued (L1 hit count)
         self.resident = False   # set by run_plan when the arena holds the whole working set
         self._sync_epoch = 0
         self._task_misses = 0
@@ -408,6 +413,13 @@ class _GpuWorker:
             if stolen is not None:
                 self.rs.put(stolen)
 
+    def _dir_version(self):
+        """Changes whenever some GPU's cache gains a tile (Eq. 3 inputs changed)."""
+        if self.ic is not None:
+            met = self.ic.metrics
+            return int(met[:, 2].sum() + met[:, 3].sum())
+        return self.runtime.directory.version
+
     def _priority(self, task: Task) -> int:
         w = self.runtime.options.critical_path_weight
         if w:
@@ -417,6 +429,13 @@ class _GpuWorker:
     def _eq3(self, task: Task) -> int:
         """Eq. 3: +2 per input-tile reference already in this GPU's L1, +1 per reference
         held by a peer of the same group (counted per step reference, scheduler.py:341-354)."""
+        if self.ic is not None:
+            tids, mult = ic_task_tiles(task)
+            local = self.ic.off[self.ic_d, tids] >= 0
+            if not self.runtime.options.l2_enabled:
+                return int(2 * mult[local].sum())
+            held = (self.ic.holders[tids] & self._ic_group) != 0
+            return int((mult * np.where(local, 2, held)).sum())
         blocks = self.cache._blocks
         holders = self.runtime.directory._holders if self.runtime.options.l2_enabled else None
         group = self._group_peers
@@ -443,7 +462,7 @@ class _GpuWorker:
         self._refill()
         # Eq. 3 only changes when some cache gains or loses a tile: recompute an entry's
         # priority only if the directory changed since it was last computed
-        ver = self.runtime.directory.version
+        ver = self._dir_version()
         for e in self.rs.entries():
             if e.pver != ver:
                 e.priority = self._priority(e.task)
@@ -772,6 +791,9 @@ class _GpuWorker:
                     self._trsm_inverse(last.key, ao, al, aw, (act.stream + 1) % self.n_streams, n)
             act.next_op = 0
             act.flops = task.flops
+            if self.ic is not None:
+                task_keys(task)
+                self._ic_refs += task._bx_refs
         finally:
             self._cur = None
         self.active[slot_index] = act
@@ -817,6 +839,23 @@ class _GpuWorker:
                         act.misses_epoch = self._sync_epoch
                     res = act.res = self._resolve_op(task, op, res)
                     act.misses_epoch = self._sync_epoch
+                elif self.ic is not None:
+                    if type(op) is GemmOp:
+                        last = i == len(ops)
+                        steps, raw = ic_op_steps(task, act.prog, i - 1, res)
+                        waits = act.pending_waits
+                        act.pending_waits = []
+                        ev = eng.ic_gemm(self.ic, self.ic_d, stream, self.f32, op.ta, op.tb, op.tri,
+                                         h, w, steps, raw, op.alpha, op.beta, act.c_off, act.c_ld,
+                                         waits, event=last)
+                        self._launched(act, ev)
+                        break
+                    if op.key not in res:     # MatOp: its diagonal tile
+                        offs, lds, wts = eng.ic_resolve(self.ic, self.ic_d,
+                                                        array("i", (ic_tile_index(task, op.key),)))
+                        res[op.key] = (offs[0], lds[0], wts[0] if wts else None)
+                        if len(wts) > 1:
+                            act.pending_waits.extend(wts[1:])
                 elif opts.l1_enabled:
                     want = (op.keys if type(op) is GemmOp else frozenset((op.key,))) - res.keys()
                     if want:
@@ -1032,7 +1071,25 @@ class _GpuWorker:
     def idle(self) -> bool:
         return all(a is None for a in self.active)
 
+    def ic_fold(self) -> None:
+        """Add this GPU's resident issue engine counters to its metrics."""
+        if self.ic is None:
+            return
+        met = self.ic.metrics[self.ic_d]
+        self.dm.h2d_bytes += int(met[0])
+        self.dm.d2d_in_bytes += int(met[1])
+        self.host_fetches += int(met[2])
+        self.l2_hits += int(met[3])
+        self.l1_hits += self._ic_refs - int(met[2] + met[3])
+        if met[4]:
+            self.runtime.add_d2d_out(self.device_id, int(met[4]))
+
     def release_all(self) -> None:
+        if self.ic is not None:
+            if self.ic_d == 0:
+                self.eng.ic_destroy(self.ic)
+            self.arena.free(self._ic_region)
+            self.ic, self.ic_d, self._ic_region = None, -1, -1
         for off, _ld, _ev, _landed in self._inv.values():
             self.arena.free(off)
         for ev in self._inv_events:
@@ -1077,6 +1134,117 @@ def critical_path(task: Task, plan: TaskPlan) -> int:
             t._bx_cp = memo[t.task_id]
         cp = task._bx_cp
     return cp
+
+
+# ---- resident issue engine (engine.ic_*): tile ids and precompiled launch operands ----
+
+IC_KINDS = ("gemm", "syrk", "syr2k", "symm")
+
+
+def ic_index(plan: TaskPlan):
+    """Input tiles of the plan's structure: (key -> tile id, [(key, phys h, phys w)]).
+    Memoised on the (shared, immutable) tasks, so repeated calls of one shape reuse it."""
+    if not plan.tasks:
+        return {}, []
+    hit = getattr(plan.tasks[0], "_bx_icmap", None)
+    if hit is not None:
+        return hit, plan.tasks[0]._bx_icgeom
+    refs = {}
+    for t in plan.tasks:
+        for k, (ref, _m) in task_keys(t).items():
+            refs.setdefault(k, ref)
+    order = sorted(refs)
+    tid = {k: i for i, k in enumerate(order)}
+    geom = [(k, refs[k].phys_height, refs[k].phys_width) for k in order]
+    for t in plan.tasks:
+        t._bx_icmap = tid
+        t._bx_icgeom = geom
+    return tid, geom
+
+
+def ic_task_tiles(task: Task):
+    """The task's distinct input tile ids and per-tile reference counts (Eq. 3)."""
+    hit = getattr(task, "_bx_ictiles", None)
+    if hit is None:
+        keys = task_keys(task)
+        tmap = task._bx_icmap
+        hit = (np.array([tmap[k] for k in keys], dtype=np.int64),
+               np.array([m for _r, m in keys.values()], dtype=np.int64))
+        task._bx_ictiles = hit
+    return hit
+
+
+def ic_tile_index(task: Task, key) -> int:
+    return task._bx_icmap[key]
+
+
+def ic_op_steps(task: Task, prog, index: int, res):
+    """Launch ``index`` of the task's program as bx_ic_gemm step rows {a, b, depth, kmode}
+    (scratch operand i -> id -(i+1), its (offset, ld) in the returned raw array)."""
+    cache = getattr(task, "_bx_icsteps", None)
+    if cache is None or cache[0] is not prog:
+        cache = (prog, {})
+        task._bx_icsteps = cache
+    hit = cache[1].get(index)
+    if hit is None:
+        tmap = task._bx_icmap
+        rows = array("i")
+        scratch = False
+        for ak, bk, d, km in prog.ops[index].subs:
+            for k in (ak, bk):
+                if k[0] == "#scratch":
+                    rows.append(-(k[1] + 1))
+                    scratch = True
+                else:
+                    rows.append(tmap[k])
+            rows.append(d)
+            rows.append(km)
+        hit = cache[1][index] = (rows, scratch)
+    rows, scratch = hit
+    raw = None
+    if scratch:
+        raw = array("q")
+        for i in range(len(prog.scratch_n)):
+            off, ld, _ = res[scratch_key(i)]
+            raw.append(off)
+            raw.append(ld)
+    return rows, raw
+
+
+def _ic_setup(plan, options, workers, engine, topology) -> None:
+    """Resident issue engine for this call: every GPU resident, L1 on, no tracing, one
+    driver process, a routine whose programs are GEMM launches (+ materialise / axpy).
+    Each GPU reserves a region of its arena for the call's input tiles."""
+    if (not hasattr(engine, "ic_create") or options.record_trace or not options.l1_enabled
+            or plan.call.kind not in IC_KINDS or plan.snapshot_alias is not None
+            or os.environ.get("BX_IC", "1") == "0" or not plan.tasks
+            or not all(w.resident for w in workers) or len(workers) > 32):
+        return
+    tmap, geom = ic_index(plan)
+    esz = plan.dtype.itemsize
+    t = plan.tile_size
+    rows = array("q")
+    region = 0
+    for (mid, i, j), h, w in geom:
+        desc = plan.matrices[mid]
+        ld = device_ld(h)
+        rows.extend((desc.element_address(i * t, j * t), desc.leading_dim, h, w, esz, ld))
+        region += -(-ld * w * esz // 256) * 256
+    offs = []
+    try:
+        for w in workers:
+            offs.append(w.arena.alloc(region))
+    except ArenaOutOfMemoryError:
+        for w, off in zip(workers, offs):
+            w.arena.free(off)
+        return
+    groups = {}
+    gid = [groups.setdefault(topology.peer_group_of(w.desc), len(groups)) for w in workers]
+    table = engine.ic_create([w.slot for w in workers], gid, rows, offs, [region] * len(workers),
+                             options.l2_enabled)
+    for d, (w, off) in enumerate(zip(workers, offs)):
+        w.ic, w.ic_d, w._ic_region = table, d, off
+        w._ic_group = sum(1 << e for e in range(len(workers)) if gid[e] == gid[d] and e != d)
 
 
 def task_keys(task: Task) -> dict:
@@ -1256,6 +1424,7 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
             w.cache.arena = w.arena
         w.runtime_trace = []
     rt.workers = workers
+    _ic_setup(plan, options, workers, engine, topology)
     for w in workers:
         w.epoch = engine.record(w.slot, 0, timing=True)
     t0 = time.perf_counter()
@@ -1271,10 +1440,17 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
                 engine.device_sync(w.slot)
             except Exception:
                 pass
+        if workers and workers[0].ic is not None:
+            try:
+                engine.ic_destroy(workers[0].ic)
+            except Exception:
+                pass
         _unpin(engine, pinned_here)
         raise
     wall = time.perf_counter() - t0
     t_fin0 = time.perf_counter()
+    for w in workers:
+        w.ic_fold()
     metrics = _finalize(rt, workers, wall)
     for w in workers:
         w.release_all()

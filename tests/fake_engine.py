@@ -46,7 +46,7 @@ class FakeEngine:
         self.ops_log = []
         self._lock = threading.RLock()
         for name in ("ensure_arenas", "register_host", "unregister_host", "h2d", "d2h", "p2p",
-                     "copy_batch", "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
+                     "copy_batch", "ic_create", "ic_resolve", "ic_gemm", "ic_destroy", "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
                      "sync", "stream_wait", "device_sync"):
             setattr(self, name, _locked(getattr(type(self), name)).__get__(self))
 
@@ -187,6 +187,107 @@ class FakeEngine:
         eh = self.record(slot, -1) if -1 in used else -1
         ep = self.record(slot, -3) if -3 in used else -1
         return eh, ep
+
+    # ---- resident issue engine (bx_ic_*) ----
+    def ic_create(self, slots, groups, tiles, region_off, region_bytes, l2):
+        return _FakeIcTable(slots, groups, tiles, region_off, region_bytes, l2)
+
+    def ic_destroy(self, table):
+        assert not table.destroyed, "ic table destroyed twice"
+        table.destroyed = True
+
+    def _ic_resolve(self, table, d, tids, waits):
+        """bx_ic_resolve semantics: missing tiles are copied from the lowest-id holder of
+        d's peer group (waiting on its arrival event) or from the host, one arrival event
+        per copy lane for the batch; pending arrival events of present tiles are waited."""
+        import ctypes
+        assert not table.destroyed
+        slot = table.slots[d]
+        new = {-1: [], -3: []}
+        seen = set()
+        for t in tids:
+            t = int(t)
+            if t in seen:
+                continue
+            seen.add(t)
+            if table.off[d, t] >= 0:
+                e = int(table.ev[d, t])
+                if e >= 0:
+                    if self.ev_done[e]:
+                        table.ev[d, t] = -1
+                    elif e not in waits:
+                        waits.append(e)
+                continue
+            host, hld, h, w, esz, ld = table.tiles[t]
+            nbytes = ld * w * esz
+            o = -(-table.cur[d] // 256) * 256
+            if o + nbytes > table.end[d]:
+                from paper_1510_05041_b200.errors import ArenaOutOfMemoryError
+                raise ArenaOutOfMemoryError("ic: resident region exhausted")
+            table.cur[d] = o + nbytes
+            table.off[d, t] = o
+            src = -1
+            if table.l2:
+                for e in range(table.ndev):
+                    if e != d and (int(table.holders[t]) >> e) & 1 and table.groups[e] == table.groups[d]:
+                        src = e
+                        break
+            payload = h * w * esz
+            if src >= 0:
+                so, sslot = int(table.off[src, t]), table.slots[src]
+                se = int(table.ev[src, t])
+
+                def fn(so=so, sslot=sslot, o=o, nbytes=nbytes):
+                    self.arenas[slot][o // 8:(o + nbytes) // 8] = self.arenas[sslot][so // 8:(so + nbytes) // 8]
+                self._enqueue(slot, -3, fn, [se] if se >= 0 else [])
+                new[-3].append(t)
+                table.metrics[d, 1] += payload
+                table.metrics[d, 3] += 1
+                table.metrics[src, 4] += payload
+            else:
+                dt = np.float64 if esz == 8 else np.float32
+                hbytes = (hld * (w - 1) + h) * esz
+
+                def fn(host=host, hld=hld, h=h, w=w, o=o, ld=ld, esz=esz, dt=dt, hbytes=hbytes):
+                    raw = np.frombuffer((ctypes.c_char * hbytes).from_address(host), dtype=dt)
+                    full = np.lib.stride_tricks.as_strided(raw, shape=(h, w), strides=(esz, hld * esz))
+                    self._viewT(slot, o, ld, h, w, esz)[:, :] = full
+                self._enqueue(slot, -1, fn, [])
+                new[-1].append(t)
+                table.metrics[d, 0] += payload
+                table.metrics[d, 2] += 1
+            table.holders[t] = int(table.holders[t]) | (1 << d)
+        for lane, lst in new.items():
+            if lst:
+                e = self.record(slot, lane)
+                for t in lst:
+                    table.ev[d, t] = e
+                waits.append(e)
+
+    def ic_resolve(self, table, d, tids):
+        waits = []
+        self._ic_resolve(table, d, tids, waits)
+        table.metrics[d, 5] += len(tids)
+        return ([int(table.off[d, t]) for t in tids], [table.tiles[t][5] for t in tids], waits)
+
+    def ic_gemm(self, table, d, stream, f32, ta, tb, tri, h, w, steps, raw, alpha, beta, c_off,
+                ldc, waits=(), event=True):
+        tids = [v for i in range(len(steps) // 4) for v in steps[4 * i:4 * i + 2] if v >= 0]
+        wts = list(waits)
+        self._ic_resolve(table, d, tids, wts)
+        table.metrics[d, 5] += len(tids)
+        rows = []
+        for i in range(len(steps) // 4):
+            a, b, dep, km = steps[4 * i:4 * i + 4]
+            ops = []
+            for v in (a, b):
+                if v >= 0:
+                    ops += [int(table.off[d, v]), table.tiles[v][5]]
+                else:
+                    ops += [raw[2 * (-v - 1)], raw[2 * (-v - 1) + 1]]
+            rows.append((ops[0], ops[1], ops[2], ops[3], dep, km))
+        return self.gemm(table.slots[d], stream, ta, tb, tri, h, w, rows, alpha, beta, c_off, ldc,
+                         wts, f32=f32, event=event)
 
     # ---- kernels ----
     def gemm(self, slot, stream, ta, tb, tri, h, w, steps, alpha, beta, c_off, ldc, waits=(),
@@ -333,3 +434,20 @@ class FakeEngine:
 
     def launches(self):
         return self.n_launches
+
+
+class _FakeIcTable:
+    """engine.IcTable stand-in: the same numpy state arrays, kept in Python."""
+
+    def __init__(self, slots, groups, tiles, region_off, region_bytes, l2):
+        n = len(tiles) // 6
+        self.ndev, self.ntiles = len(slots), n
+        self.slots, self.groups, self.l2 = list(slots), list(groups), bool(l2)
+        self.tiles = [tuple(int(v) for v in tiles[6 * t:6 * t + 6]) for t in range(n)]
+        self.off = np.full((self.ndev, n), -1, dtype=np.int64)
+        self.ev = np.full((self.ndev, n), -1, dtype=np.int64)
+        self.holders = np.zeros(n, dtype=np.int64)
+        self.metrics = np.zeros((self.ndev, 8), dtype=np.int64)
+        self.cur = list(region_off)
+        self.end = [o + b for o, b in zip(region_off, region_bytes)]
+        self.destroyed = False

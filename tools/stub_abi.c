@@ -81,3 +81,48 @@ int bx_write_flag(int d, int l, uint64_t f, uint32_t v, int nw, const int *w) { 
 int bx_atomic_add(int64_t *p, int64_t v, int64_t *old) { *old = __atomic_fetch_add(p, v, __ATOMIC_SEQ_CST); return 0; }
 int bx_atomic_cas(int64_t *p, int64_t e, int64_t d, int64_t *old) {
   int64_t x = e; __atomic_compare_exchange_n(p, &x, d, 0, __ATOMIC_SEQ_CST, __ATOMIC_SEQ_CST); *old = x; return 0; }
+/* resident issue engine: the table bookkeeping of the real library (bump allocation,
+ * holder masks, one arrival event per lane and batch), no CUDA */
+#include <stdlib.h>
+typedef struct { int ndev, nt; int64_t *off; int32_t *ev; uint32_t *hold; int64_t *met; uint64_t *cur;
+                 int64_t *tiles; uint32_t *stamp; uint32_t epoch; } IcStub;
+static IcStub *ics[64];
+int bx_ic_create(int ndev, const int *slots, const int *groups, int nt, const int64_t *tiles,
+                 const uint64_t *roff, const uint64_t *rb, int l2, int *id) {
+    IcStub *c = calloc(1, sizeof(IcStub)); c->ndev = ndev; c->nt = nt;
+    c->off = malloc(sizeof(int64_t) * ndev * nt); for (int i = 0; i < ndev * nt; ++i) c->off[i] = -1;
+    c->ev = malloc(sizeof(int32_t) * ndev * nt); for (int i = 0; i < ndev * nt; ++i) c->ev[i] = -1;
+    c->hold = calloc(nt, 4); c->met = calloc(ndev * 8, 8); c->cur = malloc(8 * ndev);
+    c->tiles = malloc(48 * (size_t)nt); memcpy(c->tiles, tiles, 48 * (size_t)nt);
+    c->stamp = calloc(nt, 4);
+    for (int d = 0; d < ndev; ++d) c->cur[d] = roff[d];
+    for (int i = 0; i < 64; ++i) if (!ics[i]) { ics[i] = c; *id = i; return 0; }
+    return 7; }
+int bx_ic_destroy(int id) { IcStub *c = ics[id]; free(c->off); free(c->ev); free(c->hold); free(c->met);
+    free(c->cur); free(c->tiles); free(c->stamp); free(c); ics[id] = 0; return 0; }
+int bx_ic_state(int id, int64_t **o, int32_t **e, uint32_t **h, int64_t **m) {
+    *o = ics[id]->off; *e = ics[id]->ev; *h = ics[id]->hold; *m = ics[id]->met; return 0; }
+static void ic_res(IcStub *c, int d, int n, const int32_t *t) {
+    int nh = 0, np = 0; ++c->epoch;
+    for (int i = 0; i < n; ++i) {
+        int x = t[i]; if (c->stamp[x] == c->epoch) continue; c->stamp[x] = c->epoch;
+        size_t idx = (size_t)d * c->nt + x;
+        if (c->off[idx] >= 0) continue;
+        const int64_t *r = c->tiles + 6 * x; uint64_t b = (uint64_t)r[5] * r[3] * r[4];
+        c->off[idx] = (int64_t)((c->cur[d] + 255) & ~255ull); c->cur[d] = c->off[idx] + b;
+        int src = -1; for (int e = 0; e < c->ndev; ++e) if (e != d && ((c->hold[x] >> e) & 1)) { src = e; break; }
+        if (src >= 0) { c->met[d * 8 + 1] += r[2] * r[3] * r[4]; c->met[d * 8 + 3]++; c->met[src * 8 + 4] += r[2] * r[3] * r[4]; ++np; }
+        else { c->met[d * 8] += r[2] * r[3] * r[4]; c->met[d * 8 + 2]++; ++nh; }
+        c->hold[x] |= 1u << d;
+    }
+    if (nh) ev_next++;
+    if (np) ev_next++; }
+int bx_ic_resolve(int id, int d, int n, const int32_t *t, int64_t *o, int32_t *l, int *nw, int *w, int cap) {
+    IcStub *c = ics[id]; ic_res(c, d, n, t);
+    for (int i = 0; i < n; ++i) { o[i] = c->off[(size_t)d * c->nt + t[i]]; l[i] = (int)c->tiles[6 * t[i] + 5]; }
+    *nw = 0; return 0; }
+int bx_ic_gemm(int id, int d, int s, int f, int ta, int tb, int tr, int h, int w, int ns, const int32_t *st,
+               const int64_t *raw, int nraw, double al, double be, uint64_t co, int lc, int n, const int *wt, int *ev) {
+    int32_t t[8192]; int k = 0; IcStub *c = ics[id];
+    for (int i = 0; i < ns; ++i) { if (st[4 * i] >= 0) t[k++] = st[4 * i]; if (st[4 * i + 1] >= 0) t[k++] = st[4 * i + 1]; }
+    ic_res(c, d, k, t); launches++; return EV(ev); }
