@@ -52,6 +52,7 @@ struct EventPool {
   std::atomic<cudaEvent_t*> chunk[kChunks] = {};
   std::atomic<int> count{0};
   std::vector<uint8_t> timing;  // guarded by mu
+  std::vector<uint8_t> in_use;  // guarded by mu: a double release would hand one event to two owners
   std::vector<int> free_sync, free_timing;
   ~EventPool() {
     for (auto& c : chunk) delete[] c.load();
@@ -61,8 +62,11 @@ struct EventPool {
     *e = chunk[idx / kChunk].load(std::memory_order_acquire)[idx % kChunk];
     return true;
   }
-  void release(int idx) {  // caller holds mu
+  bool release(int idx) {  // caller holds mu
+    if (!in_use[idx]) return false;
+    in_use[idx] = 0;
     (timing[idx] ? free_timing : free_sync).push_back(idx);
+    return true;
   }
 };
 
@@ -107,6 +111,7 @@ int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
   if (!fl.empty()) {
     idx = fl.back();
     fl.pop_back();
+    P.in_use[idx] = 1;
     P.lookup(idx, ev);
   } else {
     idx = P.count.load(std::memory_order_relaxed);
@@ -126,6 +131,7 @@ int ev_get(int d, bool timing, cudaEvent_t* ev, int* id) {
     }
     c[idx % EventPool::kChunk] = e;
     P.timing.push_back(timing ? 1 : 0);
+    P.in_use.push_back(1);
     P.count.store(idx + 1, std::memory_order_release);
     *ev = e;
   }
@@ -1258,7 +1264,7 @@ int bx_event_release(int ev) {
   EventPool& P = *g_devs[d].pool;
   std::lock_guard<std::mutex> lk(P.mu);
   if (idx >= P.count.load()) return set_err(BX_EINVAL, "bad event");
-  P.release(idx);
+  if (!P.release(idx)) return set_err(BX_EINVAL, "event " + std::to_string(ev) + " released twice");
   return BX_OK;
 }
 
@@ -1271,7 +1277,7 @@ int bx_event_release_many(int n, const int* evs) {
     EventPool& P = *g_devs[d].pool;
     std::lock_guard<std::mutex> lk(P.mu);
     if (idx >= P.count.load()) return set_err(BX_EINVAL, "bad event");
-    P.release(idx);
+    if (!P.release(idx)) return set_err(BX_EINVAL, "event " + std::to_string(ev) + " released twice");
   }
   return BX_OK;
 }

@@ -307,7 +307,7 @@ class CudaEngine:
 
     def release(self, ev) -> None:
         if ev is not None and ev >= 0:
-            self.lib.bx_event_release(ev)
+            N.check(self.lib.bx_event_release(ev), "event release")
 
     def release_many(self, evs) -> None:
         """Return several events to the pool in one call (a task's events at retirement)."""

@@ -1022,10 +1022,10 @@ class _GpuWorker:
             self.arena.free(off)
         kept = act.retained
         if kept is not None:
-            # cached at issue: the write-back has landed, so the solve has too; its event
-            # id stays allocated until the call ends (a peer may have read it as a wait)
+            # cached at issue: the write-back has landed, so the solve has too.  Its event
+            # id now belongs to the block (a peer may have read it as a wait) and is
+            # released with the block when the call ends (release_all -> _on_evict)
             kept.ready_done = True
-            self._inv_events.append(kept.ready_ev)
             act.events = [e for e in act.events if e != kept.ready_ev]
         self.eng.release_many(act.events)
         key = task.out_ref.key()

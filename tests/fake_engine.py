@@ -44,6 +44,7 @@ class FakeEngine:
         self.registered = 0
         self.flag = [False] * n_devices
         self.ops_log = []
+        self.released = set()
         self._lock = threading.RLock()
         for name in ("ensure_arenas", "register_host", "unregister_host", "h2d", "d2h", "p2p",
                      "copy_batch", "ic_create", "ic_resolve", "ic_gemm", "ic_destroy", "gemm", "trsm", "trsm_inverse", "trsm_apply", "materialize", "singular", "record", "done", "wait_any",
@@ -92,6 +93,7 @@ class FakeEngine:
         ev = self._new_ev()
         for w in waits:
             assert w in self.ev_done, f"wait on unknown event {w}"
+            assert w not in self.released, f"wait on released event {w}"
         self.queues.setdefault((slot, lane), []).append((list(waits), fn, ev, cond))
         return ev
 
@@ -398,6 +400,7 @@ class FakeEngine:
         return self._enqueue(slot, lane, lambda: None, ())
 
     def done(self, ev):
+        assert ev not in self.released, f"query of released event {ev}"
         # make progress a random amount, then answer
         for _ in range(self.rng.randint(0, 3)):
             if not self._step():
@@ -421,10 +424,15 @@ class FakeEngine:
         return 1.0
 
     def release(self, ev):
-        pass
+        # the real pool recycles ids: a double release hands one event to two owners, and a
+        # released id may already name someone else's event
+        if ev is not None and ev >= 0:
+            assert ev not in self.released, f"event {ev} released twice"
+            self.released.add(ev)
 
     def release_many(self, evs):
-        pass
+        for ev in evs:
+            self.release(ev)
 
     def stream_wait(self, slot, lane, ev):
         self._enqueue(slot, lane, lambda: None, (ev,))
