@@ -1,6 +1,6 @@
 """Timeline analysis of one host-resident call (record_trace=True): where does e2e time go?
 python tools/trace_e2e.py [n] [tile] [chunk] [tasks_per_stream] [first_chunk]
-(BX_KIND=gemm|syrk|syr2k|trsm|trmm, BX_F32=1 for SGEMM)"""
+(BX_KIND=gemm|syrk|syr2k|trsm|trmm, BX_K=depth, BX_F32=1 for SGEMM; chunk 0 = auto)"""
 import sys
 import time
 
@@ -12,12 +12,12 @@ from paper_1510_05041_b200.engine import get_engine
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 t = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
-chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # 0 = auto
 tps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
-fc = int(sys.argv[5]) if len(sys.argv) > 5 else 4
+fc = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 import os
 kind = os.environ.get("BX_KIND", "gemm")
-call = build_call(kind, m=n, n=n, k=n, tile_size=t, seed=0, alpha=1.0,
+call = build_call(kind, m=n, n=n, k=int(os.environ.get("BX_K", n)), tile_size=t, seed=0, alpha=1.0,
                   beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0, uplo="lower",
                   trsm_scaled=True, **({"dtype": np.float32} if os.environ.get("BX_F32") else {}))
 eng = get_engine([0])
