@@ -63,7 +63,8 @@ def scratch_key(i: int) -> tuple:
 
 
 def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
-                 defer_c: bool = False) -> Program:
+                 defer_c: bool = False, split_chain: bool = False,
+                 split_km: bool = False) -> Program:
     """``first_chunk`` (if > 0) caps the task's first GEMM launch so its kernel can start
     as soon as the first few input tiles have landed (pipeline ramp-up).
 
@@ -71,8 +72,19 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
     GEMM updates, no triangle epilogue, no solve), the first GEMM launch runs with beta = 0
     (C is not read, kernels.py:40-41) and a final AxpyOp adds beta*C0 from a separately
     fetched copy — beta is still applied exactly once (routines.py:211-215), but the
-    task's kernels no longer wait for the C tile's host copy."""
-    ckey = (chunk_steps, first_chunk, defer_c)
+    task's kernels no longer wait for the C tile's host copy.
+
+    ``split_chain`` (TRSM): when the task's last update step reads the tile its chain
+    predecessor solves (k adjacent to the diagonal: left/lower and right/upper, whose
+    updates run towards the diagonal, routines.py:347-375), that step gets a launch of its
+    own.  The earlier updates read tiles solved long before, so their launch can start
+    while the predecessor's solve is still running; only the one-step launch and the solve
+    wait for it.  Same steps, same order, same beta: the numerics are unchanged.
+
+    ``split_km``: a triangular-operand step (TRMM diagonal) never shares a launch with
+    plain steps, so the plain steps run the kernel instantiation without per-step k-range
+    bookkeeping (bx_gemm_dmma.cuh KM template) — same steps and order."""
+    ckey = (chunk_steps, first_chunk, defer_c, split_chain, split_km)
     cache = getattr(task, "_bx_prog", None)
     if cache is not None and cache[0] == ckey:
         return cache[1]
@@ -98,13 +110,21 @@ def compile_task(task: Task, call, chunk_steps: int, first_chunk: int = 0,
         if first_chunk and not any(type(o) is GemmOp for o in ops):
             cap = min(first_chunk, chunk_steps)
         if (cur is None or (cur[0], cur[1], cur[2], cur[3]) != (ta, tb, tr, alpha)
-                or beta != 1.0 or len(cur[5]) >= cap):
+                or beta != 1.0 or len(cur[5]) >= cap
+                or (split_km and (km != KM_NONE) != (cur[5][-1][3] != KM_NONE))):
             flush()
             cur = [ta, tb, tr, alpha, beta, [], k]
         cur[5].append((a, b, d, km))
 
-    for st in task.steps:
+    split_at = -1
+    if split_chain and len(task.steps) >= 3 and task.steps[-1].kind == TRSM_SOLVE:
+        last = task.steps[-2]
+        if last.kind == GEMM_UPDATE and abs(last.k - task.steps[-1].k) == 1:
+            split_at = len(task.steps) - 2
+    for si, st in enumerate(task.steps):
         kind = st.kind
+        if si == split_at:
+            flush()
         if kind == GEMM_UPDATE:
             add(st.a.transposed, st.b.transposed, 0, st.alpha, st.beta, st.a.key(), st.b.key(),
                 st.a.width, st.k)

@@ -104,6 +104,16 @@ class RunOptions:
                                        # write-back + a host poll (the write-back still
                                        # completes the task).  False = the reference's
                                        # release-after-write-back
+    trsm_split_chain: bool = False     # TRSM: the update step reading the chain
+                                       # predecessor's solved tile gets its own launch, so
+                                       # the task's other updates need not wait for that
+                                       # solve (program.compile_task).  Measured slower on
+                                       # cfg4: 139.1 vs 135.5 ms (profiles/trsm_ab_r02.txt)
+    split_km: bool = False             # TRMM: the diagonal (triangular-operand) step gets
+                                       # its own launch, so the plain steps skip the k-range
+                                       # bookkeeping of the KM kernel instantiation.
+                                       # Measured slower on cfg4 TRMM: 139.2 vs 136.7 ms
+                                       # (profiles/trmm_syrk_ab_r02.txt)
     trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
                                        # (resident arenas): X = alpha inv(E) B with inv(E)
                                        # computed once per diagonal tile; 0 = substitution
@@ -760,7 +770,8 @@ class _GpuWorker:
                 act.ramp = True
                 chunk = min(opts.ramp_chunk_steps, chunk)
             act.prog = compile_task(task, self.plan.call, chunk, opts.first_chunk_steps,
-                                    opts.defer_c_move_in)
+                                    opts.defer_c_move_in, opts.trsm_split_chain,
+                                    opts.split_km)
             if act.prog.defer_c:
                 # C0 gets its own buffer, fetched with the task's last launch group
                 act.c_pending = False

@@ -432,3 +432,66 @@ def test_resident_issue_engine_off_paths():
                            for i in range(2)])
         run_call(call, topo_r, opts, engine=eng)
         assert calls == {"gemm": 0, "resolve": 0}, (kind, opts)
+
+
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "trsm"], ids=lambda c: c["name"])
+def test_trsm_split_chain_matches_reference(case, split):
+    """RunOptions.trsm_split_chain: the update step that reads the chain predecessor's
+    solved tile runs as its own launch (program.compile_task) — same results on every
+    side / uplo / trans / diag variant, with and without release-on-issue."""
+    from paper_1510_05041_b200.program import GemmOp, TrsmOp, compile_task
+    call = call_of(case)
+    eng = FakeEngine(2, seed=len(case["name"]) + 3, arena_bytes=1 << 24)
+    topo_r = Topology([DeviceDesc(i, peer_group="g") for i in range(2)])
+    res = run_call(call, topo_r, RunOptions(chunk_steps=4, trsm_split_chain=split), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-10, atol=1e-10)
+    pc = res.plan.call
+    for t in res.plan.tasks:
+        prog = compile_task(t, pc, 4, 0, False, split)
+        gemms = [o for o in prog.ops if type(o) is GemmOp]
+        assert type(prog.ops[-1]) is TrsmOp
+        n_upd = len(t.steps) - 1
+        assert sum(len(g.subs) for g in gemms) == n_upd          # every update step, once
+        toward = n_upd >= 2 and abs(t.steps[-2].k - t.steps[-1].k) == 1
+        if split and toward:
+            assert len(gemms[-1].subs) == 1 and gemms[-1].subs[0][0] == t.steps[-2].a.key()
+            assert len(gemms) == -(-(n_upd - 1) // 4) + 1
+        else:
+            assert len(gemms) == -(-n_upd // 4)
+
+
+def test_trsm_split_chain_cfg4_shape():
+    """cfg4 (left / lower / notrans): task (i, j) updates k = 0..i-1 then solves; with the
+    split its last launch is the k = i-1 step alone."""
+    from paper_1510_05041_b200.program import GemmOp, compile_task
+    call = build_call("trsm", m=64, n=32, k=64, tile_size=8, seed=1, uplo="lower", trsm_scaled=True)
+    from paper_1510_05041_b200.routines import generate_tasks
+    plan = generate_tasks(call)
+    for t in plan.tasks:
+        i = t.out_ref.i
+        prog = compile_task(t, call, 16, 0, False, True)
+        gemms = [o for o in prog.ops if type(o) is GemmOp]
+        if i >= 2:
+            assert [len(g.subs) for g in gemms] == [i - 1, 1]
+        elif i == 1:
+            assert [len(g.subs) for g in gemms] == [1]
+        else:
+            assert gemms == []
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "trmm"], ids=lambda c: c["name"])
+def test_split_km_trmm_matches_reference(case):
+    """RunOptions.split_km: TRMM diagonal (triangular-operand) steps run as launches of
+    their own; plain steps never share a launch with them; same results."""
+    from paper_1510_05041_b200.program import KM_NONE, GemmOp, compile_task
+    call = call_of(case)
+    eng = FakeEngine(2, seed=len(case["name"]) + 11, arena_bytes=1 << 24)
+    topo_r = Topology([DeviceDesc(i, peer_group="g") for i in range(2)])
+    res = run_call(call, topo_r, RunOptions(chunk_steps=4, split_km=True), engine=eng)
+    np.testing.assert_allclose(call.c.matrix.as_2d(), case["out"], rtol=1e-10, atol=1e-10)
+    for t in res.plan.tasks:
+        prog = compile_task(t, res.plan.call, 4, 0, False, False, True)
+        for g in (o for o in prog.ops if type(o) is GemmOp):
+            kms = {km != KM_NONE for _, _, _, km in g.subs}
+            assert len(kms) == 1
