@@ -105,6 +105,17 @@ def test_auto_launch_shape(kind, k, ndev, chunk, streams):
     o = resolve_ramp(plan, resolve_streams(plan, RunOptions(), ndev), ndev)
     assert (o.chunk_steps, o.n_streams) == (chunk, streams)
     assert 0 <= o.ramp_tasks <= max(0, len(plan.tasks) // (4 * ndev))
+    if kind == "gemm":
+        assert o.ramp_tasks == min(32, 256 // (4 * ndev))
     # explicit values are kept
     o2 = resolve_streams(plan, RunOptions(chunk_steps=3, n_streams=2), ndev)
     assert (o2.chunk_steps, o2.n_streams) == (3, 2)
+
+
+def test_no_start_up_batch_for_small_calls():
+    """cfg1-sized calls (16 tasks) issue whole-task launches from the start."""
+    call = build_call("gemm", m=256, n=256, k=256, tile_size=64, seed=0, beta=1.0)
+    plan = generate_tasks(call)
+    assert len(plan.tasks) == 16
+    assert resolve_ramp(plan, RunOptions(), 1).ramp_tasks == 0
+    assert resolve_ramp(plan, RunOptions(ramp_tasks=4), 1).ramp_tasks == 4
