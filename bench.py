@@ -487,8 +487,9 @@ def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parit
         "roofline": {"bound": "tensor", "achieved": kern["tflops"], "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": kern["tflops"] / peak_tf,
                      "traffic": kern.get("traffic"),
-                     "kernel": ("bx::sgemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 "
-                                "pair tile, TMEM accumulators, TMA)" if f32 else
+                     "kernel": ("bx::sgemm_tc2c_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 "
+                                "pair tiles taken by cluster launch control, double-buffered TMEM "
+                                "accumulators, TMA)" if f32 else
                                 "bx::gemm_task_mb_kernel (FP64 DMMA m8n8k4, mbarrier cp.async ring)"),
                      "kernel_shape": kern["shape"], "flops_per_launch": kern["flops"],
                      "avg_launch_ms": kern["ms"], "peak_source": peak_src,

@@ -166,8 +166,10 @@ int bx_set_gemm_group(int group);
 int bx_set_trsm_leaf(int n);
 /* tuning knob: right-hand sides per CTA of the TRSM panel kernel (8, 16, 32 or 64; default 32) */
 int bx_set_trsm_rhs(int nr);
-/* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile
- * (default), 2 = persistent 2-SM with double-buffered TMEM accumulators */
+/* tuning knob: SGEMM kernel, 0 = 1-SM 128x256 tile, 1 = 2-SM (cta_group::2) 256x256 tile,
+ * 2 = persistent 2-SM with double-buffered TMEM accumulators (static round robin),
+ * 3 = the same persistent kernel taking tiles by cluster launch control (launch order;
+ * default) */
 int bx_set_sgemm_variant(int variant);
 /* tuning knob: load MN-major SGEMM operands with one 3-d TMA box per stage (1, default) or
  * one 2-d box per 32-wide group (0) */

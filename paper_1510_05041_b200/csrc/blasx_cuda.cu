@@ -349,8 +349,10 @@ int tensor_map_f32_mn3d(const float* base, uint64_t rows, uint64_t cols, uint64_
   return BX_OK;
 }
 
-int g_sgemm_variant = 1;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile (default),
+int g_sgemm_variant = 3;   // 0: 1-SM 128x256 tile, 1: 2-SM pair 256x256 tile,
                            // 2: persistent 2-SM with double-buffered TMEM accumulators
+                           // (static round robin), 3: the same with cluster launch control
+                           // (default: 98 % tensor pipe, profiles/sgemm_clc_r02.txt)
 int g_sm_pairs = 74;       // clusters of the persistent SGEMM (one per TPC of a B200)
 int g_sgemm_group = 0;     // persistent SGEMM raster group (m-tiles); 0 = kernel default
 int g_sgemm_mn3d = 1;      // MN-major operands by one 3-d TMA box when the extent allows
@@ -451,6 +453,19 @@ int sgemm_tf32(cudaStream_t s, int ta, int tb, int h, int w, int nsteps, const f
       const int pair_tiles = ((h + bx::P_BM - 1) / bx::P_BM) * ((w + bx::P_BN - 1) / bx::P_BN);
       const int clusters = pair_tiles < g_sm_pairs ? pair_tiles : g_sm_pairs;
       k3<<<2 * clusters, bx::P_THREADS, bx::P_SMEM_BYTES, s>>>(t);
+      g_launches++;
+      CUDA_TRY(cudaGetLastError());
+      if (nsteps <= 0) break;
+      continue;
+    }
+    if (g_sgemm_variant == 3) {
+      void (*k4)(bx::SgemmTask) = ta ? (tb ? bx::sgemm_tc2c_kernel<1, 1> : bx::sgemm_tc2c_kernel<1, 0>)
+                                     : (tb ? bx::sgemm_tc2c_kernel<0, 1> : bx::sgemm_tc2c_kernel<0, 0>);
+      if (need_attr((const void*)k4)) {
+        CUDA_TRY(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, bx::P_SMEM_BYTES));
+      }
+      int pairs = ((h + bx::P_BM - 1) / bx::P_BM) * ((w + bx::P_BN - 1) / bx::P_BN);
+      k4<<<2 * pairs, bx::C_THREADS, bx::P_SMEM_BYTES, s>>>(t);
       g_launches++;
       CUDA_TRY(cudaGetLastError());
       if (nsteps <= 0) break;
@@ -1385,7 +1400,7 @@ int bx_set_gemm_variant(int v) {
 }
 
 int bx_set_sgemm_variant(int v) {
-  if (v < 0 || v > 2) return set_err(BX_EINVAL, "sgemm variant must be 0, 1 or 2");
+  if (v < 0 || v > 3) return set_err(BX_EINVAL, "sgemm variant must be 0, 1, 2 or 3");
   g_sgemm_variant = v;
   return BX_OK;
 }

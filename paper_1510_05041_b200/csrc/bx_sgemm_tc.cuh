@@ -693,6 +693,278 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 }  // namespace bx
 
 // ---------------------------------------------------------------------------------------
+// Persistent 2-SM variant with cluster launch control (bx_set_sgemm_variant(3)).  The grid
+// is the full one-cluster-per-pair-tile grid of variant 1; a running cluster finishes its
+// own tile and then *cancels* the next not-yet-launched cluster (clusterlaunchcontrol.
+// try_cancel) and computes that cluster's tile instead.  The hardware hands out clusters
+// in launch order, so the in-flight tiles stay the contiguous raster window of variant 1
+// (no drift, no extra DRAM traffic — the failure of the round-robin variant 2) while the
+// double-buffered TMEM accumulators of variant 2 overlap tile t's epilogue with tile
+// t+1's MMAs.  Warp 6 of the leader CTA is the scheduler: it keeps up to two responses
+// ahead in a 2-slot ring (cfull: the response landed, multicast to both CTAs with 16
+// bytes of transaction each; cempty: all 11 consumers of the pair — 2 producers, the MMA
+// thread, 8 epilogue warps — read it, counted on the leader's barrier).  A failed cancel
+// (no cluster left) ends every role after its current tile; no query follows a failure.
+// ---------------------------------------------------------------------------------------
+namespace bx {
+
+constexpr int C_THREADS = 224;             // P_THREADS + the scheduler warp
+constexpr int C_CONSUMERS = 11;            // 2 producers + 1 MMA + 8 epilogue warps
+
+__device__ __forceinline__ uint32_t p_rank_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(s_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void p_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n"
+               ::"r"(cluster_addr), "r"(bytes) : "memory");
+}
+// cancel the next unlaunched cluster; the 16-byte response lands in every CTA of this
+// cluster at `resp`'s offset and completes 16 bytes of transaction on each CTA's `bar`
+__device__ __forceinline__ void clc_try_cancel(void* resp, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128 [%0], [%1];\n"
+      ::"r"(s_u32(resp)), "r"(s_u32(bar)) : "memory");
+}
+// ctaid.x of the first CTA of the cancelled cluster, or -1 (nothing left to cancel)
+__device__ __forceinline__ int clc_first_ctaid(const void* resp) {
+  uint32_t x = 0, ok = 0;
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b128 r;\n ld.shared.b128 r, [%2];\n"
+      " clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n selp.u32 %1, 1, 0, p;\n"
+      " @p clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, _, _, _}, r;\n}\n"
+      : "=r"(x), "=r"(ok) : "r"(s_u32(resp)) : "memory");
+  // order this generic-proxy read before the next async-proxy write of the slot
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  return ok ? (int)x : -1;
+}
+
+template <int TA, int TB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
+    sgemm_tc2c_kernel(const __grid_constant__ SgemmTask t) {
+  extern __shared__ __align__(1024) uint8_t s_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)s_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;            // [2] (used in the leader CTA)
+  uint64_t* cfull = tempty + 2;            // [2] CLC response landed
+  uint64_t* cempty = cfull + 2;            // [2] CLC response consumed (leader CTA)
+  uint4* resp = (uint4*)(cempty + 2);      // [2] 16-byte CLC responses (16-B aligned)
+  uint32_t* tmem_slot = (uint32_t*)(resp + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = p_cluster_rank();
+  const int GROUP_M = t.group_m > 0 ? t.group_m : 4;
+  const int tiles_m = (t.h + P_BM - 1) / P_BM, tiles_n = (t.w + P_BN - 1) / P_BN;
+  const int per_group = GROUP_M * tiles_n;
+  auto tile_origin = [&](int tile, int& m0, int& n0) {
+    const int first_m = (tile / per_group) * GROUP_M;
+    const int gsize = min(tiles_m - first_m, GROUP_M);
+    m0 = (first_m + (tile % per_group) % gsize) * P_BM;
+    n0 = ((tile % per_group) / gsize) * P_BN;
+  };
+  const uint32_t lead_cempty[2] = {p_leader_addr(&cempty[0]), p_leader_addr(&cempty[1])};
+  // the tile after the j-th: wait for response j, hand the slot back, decode
+  auto next_tile = [&](int j, bool release) -> int {
+    const int sl = j & 1;
+    p_mbar_wait(&cfull[sl], (j >> 1) & 1);
+    const int x = clc_first_ctaid(&resp[sl]);
+    if (release) p_arrive_cluster(lead_cempty[sl]);
+    return x < 0 ? -1 : x >> 1;
+  };
+
+  int kslabs = 0;
+  for (int s = 0; s < t.nsteps; ++s) kslabs += (t.steps[s].d + P_BK - 1) / P_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) { s_mbar_init(&full[s], 1); s_mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) {
+      s_mbar_init(&tfull[b], 1);
+      s_mbar_init(&tempty[b], 8);
+      s_mbar_init(&cfull[b], 1);
+      s_mbar_init(&cempty[b], C_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(tmem_slot)), "n"(2 * S_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  s_fence_before();
+  p_cluster_sync();
+  s_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 6) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t peer_cfull[2] = {p_rank_addr(&cfull[0], 1), p_rank_addr(&cfull[1], 1)};
+      for (int i = 0;; ++i) {
+        const int sl = i & 1;
+        if (i >= 2) p_mbar_wait(&cempty[sl], ((i >> 1) - 1) & 1);
+        s_mbar_expect_tx(&cfull[sl], 16);
+        p_arrive_expect_tx_cluster(peer_cfull[sl], 16);
+        clc_try_cancel(&resp[sl], &cfull[sl]);
+        p_mbar_wait(&cfull[sl], (i >> 1) & 1);
+        if (clc_first_ctaid(&resp[sl]) < 0) break;   // nothing left: never query again
+      }
+    }
+  } else if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x >> 1, j = 0; tile >= 0; tile = next_tile(j++, true)) {
+        if (kslabs == 0) continue;
+        int m0, n0;
+        tile_origin(tile, m0, n0);
+        const int my_m0 = m0 + 128 * (int)rank, my_n0 = n0 + 128 * (int)rank;
+        int step = 0, k0 = 0, dcur = t.steps[0].d;
+        const CUtensorMap* ma = &t.steps[0].map_a;
+        const CUtensorMap* mb = &t.steps[0].map_b;
+        for (int ks = 0; ks < kslabs; ++ks, ++it) {
+          const int st = it % P_STAGES;
+          if (it >= P_STAGES) p_mbar_wait(&empty[st], ((it / P_STAGES) - 1) & 1);
+          uint8_t* sa = smem + st * P_STAGE_BYTES;
+          uint8_t* sb = sa + P_A_BYTES;
+          if (rank == 0) s_mbar_expect_tx(&full[st], 2 * P_STAGE_BYTES);
+          if (TA) {
+            p_tma_2d_pair(sa, ma, &full[st], k0, my_m0);
+          } else if (t.a3d) {
+            p_tma_3d_pair(sa, ma, &full[st], 0, k0, my_m0 / 32);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p_tma_2d_pair(sa + i * 4096, ma, &full[st], my_m0 + 32 * i, k0);
+          }
+          if (!TB) {
+            p_tma_2d_pair(sb, mb, &full[st], k0, my_n0);
+          } else if (t.b3d) {
+            p_tma_3d_pair(sb, mb, &full[st], 0, k0, my_n0 / 32);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p_tma_2d_pair(sb + i * 4096, mb, &full[st], my_n0 + 32 * i, k0);
+          }
+          k0 += P_BK;
+          if (k0 >= dcur) {
+            k0 = 0;
+            if (++step < t.nsteps) {
+              dcur = t.steps[step].d;
+              ma = &t.steps[step].map_a;
+              mb = &t.steps[step].map_b;
+            }
+          }
+        }
+      }
+      // producer tail: the leader's last multicast commits land on this CTA's "empty"
+      // barriers before it exits (else they would hit the next CTA on this SM)
+      for (int i2 = it > P_STAGES ? it - P_STAGES : 0; i2 < it; ++i2)
+        p_mbar_wait(&empty[i2 % P_STAGES], (i2 / P_STAGES) & 1);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = (s_idesc(!TA, TB) & ~(0x1Fu << 24)) | ((uint32_t)(P_BM >> 4) << 24);
+      const uint32_t sbase = s_u32(smem);
+      const uint64_t da0 = TA ? s_desc(sbase, 16, 1024, 2) : s_desc(sbase, t.mn_lbo, t.mn_sbo, 1);
+      const uint64_t db0 = TB ? s_desc(sbase + P_A_BYTES, t.mn_lbo, t.mn_sbo, 1)
+                              : s_desc(sbase + P_A_BYTES, 16, 1024, 2);
+      constexpr uint32_t AK = TA ? 32 / 16 : 1024 / 16;
+      constexpr uint32_t BKS = TB ? 1024 / 16 : 32 / 16;
+      constexpr uint32_t SU = P_STAGE_BYTES / 16;
+      int it = 0, n = 0;
+      for (int tile = blockIdx.x >> 1, j = 0; tile >= 0; tile = next_tile(j++, true), ++n) {
+        if (kslabs == 0) continue;
+        const int b = n & 1;
+        if (n >= 2) p_mbar_wait(&tempty[b], ((n >> 1) - 1) & 1);   // epilogue drained acc b
+        s_fence_after();
+        const uint32_t acc_tm = tmem + (uint32_t)(b * S_TMEM_COLS);
+        for (int ks = 0; ks < kslabs; ++ks, ++it) {
+          const int st = it % P_STAGES;
+          p_mbar_wait(&full[st], (it / P_STAGES) & 1);
+          s_fence_after();
+          const uint64_t so = (uint64_t)(st * SU);
+#pragma unroll
+          for (int kk = 0; kk < P_BK / 8; ++kk) {
+            const uint32_t acc = (ks + kk) != 0;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                ::"r"(acc_tm), "l"(da0 + so + kk * AK), "l"(db0 + so + kk * BKS), "n"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                       ::"r"(s_u32(&empty[st])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                     ::"r"(s_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+      }
+    }
+  } else if (warp >= 2 && warp <= 5) {
+    const int q = warp & 3;
+    const uint32_t lead_tempty[2] = {p_leader_addr(&tempty[0]), p_leader_addr(&tempty[1])};
+    int n = 0;
+    for (int tile = blockIdx.x >> 1, j = 0; tile >= 0; ++n) {
+      const int b = n & 1;
+      int m0, n0;
+      tile_origin(tile, m0, n0);
+      const int row = m0 + 128 * (int)rank + 32 * q + lane;
+      if (kslabs > 0) {
+        p_mbar_wait(&tfull[b], (n >> 1) & 1);
+        s_fence_after();
+      }
+      for (int c0 = 0; c0 < P_BN; c0 += 16) {
+        uint32_t v[16];
+        if (kslabs > 0) {
+          const uint32_t taddr = tmem + (uint32_t)(b * S_TMEM_COLS) + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0u;
+        }
+        if (c0 + 16 >= P_BN && kslabs > 0) {
+          // every TMEM read of accumulator b by this warp is done: hand it back to the MMA
+          s_fence_before();
+          __syncwarp();
+          if (lane == 0) p_arrive_cluster(lead_tempty[b]);
+        }
+        if (row < t.h) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = n0 + c0 + i;
+            if (col < t.w) {
+              float* p = t.c + (size_t)col * t.ldc + row;
+              float r = t.alpha * __uint_as_float(v[i]);
+              if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
+              *p = r;
+            }
+          }
+        }
+      }
+      // next tile: every lane reads the response, one arrival per warp
+      {
+        const int sl = j & 1;
+        p_mbar_wait(&cfull[sl], (j >> 1) & 1);
+        const int x = clc_first_ctaid(&resp[sl]);
+        __syncwarp();
+        if (lane == 0) p_arrive_cluster(lead_cempty[sl]);
+        ++j;
+        tile = x < 0 ? -1 : x >> 1;
+      }
+    }
+  }
+  s_fence_before();
+  p_cluster_sync();
+  if (warp == 1) {
+    s_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * S_TMEM_COLS));
+  }
+}
+
+}  // namespace bx
+
+// ---------------------------------------------------------------------------------------
 // 3xTF32 split for the precise SGEMM mode (bx_set_sgemm_precise): x = hi + lo with hi the
 // TF32-rounded value (low 13 mantissa bits zero, so the tensor core takes it exactly) and
 // lo = x - hi (exact in fp32).  A*B ~= hi_a*hi_b + hi_a*lo_b + lo_a*hi_b restores ~fp32

@@ -231,7 +231,8 @@ def test_concurrent_mode_and_trace():
 @pytest.mark.parametrize("variant,mn3d,shape", [(1, 1, (1500, 1300, 1100)), (0, 1, (1500, 1300, 1100)),
                                                 (1, 1, (1536, 1280, 1024)), (0, 1, (1536, 1280, 1024)),
                                                 (1, 0, (1536, 1280, 1024)), (2, 1, (1500, 1300, 1100)),
-                                                (2, 1, (4608, 4352, 1024))])
+                                                (2, 1, (4608, 4352, 1024)), (3, 1, (1500, 1300, 1100)),
+                                                (3, 0, (1536, 1280, 1024)), (3, 1, (4608, 4352, 1024))])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 def test_sgemm_tcgen05_against_fp64_oracle(ta, tb, variant, mn3d, shape):
     """SGEMM has no reference path (tiling.py:57-60 is float64 only): compare with the
@@ -245,7 +246,7 @@ def test_sgemm_tcgen05_against_fp64_oracle(ta, tb, variant, mn3d, shape):
     try:
         _sgemm_case(ta, tb, *shape)
     finally:
-        lib.bx_set_sgemm_variant(1)
+        lib.bx_set_sgemm_variant(3)
         lib.bx_set_sgemm_mn3d(1)
 
 
@@ -456,3 +457,30 @@ def test_sgemm_precise_mode_meets_fp32_bound_at_small_k(i):
                              c0_norm=np.linalg.norm(c0), eps=float(np.finfo(np.float32).eps))
     assert r <= tolerance.BOUND, (r, m, n, k)
 
+
+
+@pytest.mark.parametrize("kind,kw,opts", [
+    ("trsm", dict(uplo="lower", side="left"), dict(trsm_split_chain=True)),
+    ("trsm", dict(uplo="upper", side="right", trans_a=True), dict(trsm_split_chain=True)),
+    ("trsm", dict(uplo="lower", side="left"), dict(release_on_issue=False, trsm_inverse_min=0)),
+    ("trmm", dict(uplo="lower", side="left"), dict(split_km=True)),
+    ("trmm", dict(uplo="upper", side="right", trans_a=True), dict(split_km=True, chunk_steps=2)),
+    ("gemm", dict(beta=1.0), dict(ramp_tasks=0)),
+    ("gemm", dict(beta=1.0), dict(ramp_tasks=8, ramp_chunk_steps=1)),
+])
+def test_launch_shape_options_on_hardware(kind, kw, opts):
+    """The launch-shape knobs (chain split, KM split, substitution path with the reference's
+    release rule, start-up batch on/off) on the real kernels: same north-star bound."""
+    n, k, t = 1300, 1100, 256
+    call = build_call(kind, m=n, n=n, k=k, tile_size=t, seed=11, trsm_scaled=True, **kw)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    run_call(call, options=RunOptions(**opts))
+    out = call.c.matrix.as_2d()
+    p = dict(kw)
+    alpha, beta = p.pop("alpha", 1.0), p.pop("beta", 0.0)
+    ref = c0.copy()
+    tiled.run_tiled(kind, a, ref, b, tile_size=t, alpha=alpha, beta=beta, **p)
+    r = _ratio(kind, out, ref, a, b, c0, alpha, beta, k if kind == "gemm" else n)
+    assert r <= tolerance.BOUND, r

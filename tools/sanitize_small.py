@@ -38,14 +38,14 @@ def tri(a, uplo, trans=False, unit=False):
 
 
 def sgemm(lib):
-    for variant in [int(v) for v in os.environ.get("BX_SAN_SGEMM", "0,1,2").split(",") if v]:
+    for variant in [int(v) for v in os.environ.get("BX_SAN_SGEMM", "0,1,2,3").split(",") if v]:
         lib.bx_set_sgemm_variant(variant)
         for precise in (False, True):
             call = build_call("gemm", m=600, n=520, k=512, tile_size=256, seed=6, beta=1.0,
                               dtype=np.float32)
             check(f"sgemm variant={variant} precise={precise}", call,
                   RunOptions(chunk_steps=2, sgemm_precise=precise), lambda a, b, c: a @ b + c, 2e-3)
-    lib.bx_set_sgemm_variant(1)
+    lib.bx_set_sgemm_variant(3)
 
 
 def main():
