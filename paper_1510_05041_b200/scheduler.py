@@ -117,6 +117,9 @@ class RunOptions:
     trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
                                        # (resident arenas): X = alpha inv(E) B with inv(E)
                                        # computed once per diagonal tile; 0 = substitution
+    prefetch: int = -1                 # 1: load every input tile at the call's start in
+                                       # first-use order (one GPU, resident issue engine);
+                                       # -1 = auto (calls of < SMALL_CALL_TASKS tasks), 0 off
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -1258,6 +1261,33 @@ def _ic_setup(plan, options, workers, engine, topology) -> None:
         w._ic_group = sum(1 << e for e in range(len(workers)) if gid[e] == gid[d] and e != d)
 
 
+SMALL_CALL_TASKS = 64    # below this a call has no start-up batch and may prefetch
+
+
+def _ic_prefetch(plan, options, workers, engine) -> None:
+    """Small calls on one GPU (RunOptions.prefetch, auto: fewer than SMALL_CALL_TASKS
+    tasks): enqueue every input tile's host load at the start, in the order the tasks will
+    first read them (FIFO task order, then step order), one arrival event per task's new
+    tiles.  The H2D lane then streams back to back instead of following the host's task
+    issue rate; launches find the tiles present (or in flight: they wait on the arrival
+    event).  Only with the resident issue engine on a single GPU: with several GPUs which
+    GPU needs which tile is decided dynamically (stations, stealing), and a large call's
+    C tiles would queue behind the whole prefetch on the one H2D lane."""
+    want = options.prefetch
+    if want < 0:
+        want = len(plan.tasks) < SMALL_CALL_TASKS
+    if not want or len(workers) != 1 or workers[0].ic is None:
+        return
+    w = workers[0]
+    seen = set()
+    for task in plan.tasks:
+        tids, _mult = ic_task_tiles(task)
+        new = [int(t) for t in tids if int(t) not in seen]
+        if new:
+            seen.update(new)
+            engine.ic_resolve(w.ic, w.ic_d, array("i", new))
+
+
 def task_keys(task: Task) -> dict:
     """Distinct input tiles of a task: key -> (ref, number of step references).  Cached on
     the (immutable) task together with its key set, total reference count and whether
@@ -1335,7 +1365,7 @@ def resolve_ramp(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOpti
         return options
     import dataclasses
     ntasks = len(plan.tasks)
-    ramp = min(32, ntasks // (4 * max(1, n_devices))) if ntasks >= 64 else 0
+    ramp = min(32, ntasks // (4 * max(1, n_devices))) if ntasks >= SMALL_CALL_TASKS else 0
     return dataclasses.replace(options, ramp_tasks=ramp if ramp >= 4 else 0)
 
 
@@ -1441,6 +1471,7 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
     _ic_setup(plan, options, workers, engine, topology)
     for w in workers:
         w.epoch = engine.record(w.slot, 0, timing=True)
+    _ic_prefetch(plan, options, workers, engine)
     t0 = time.perf_counter()
     t_setup = t0 - t_setup0
     try:

@@ -467,6 +467,10 @@ def test_sgemm_precise_mode_meets_fp32_bound_at_small_k(i):
     ("trmm", dict(uplo="upper", side="right", trans_a=True), dict(split_km=True, chunk_steps=2)),
     ("gemm", dict(beta=1.0), dict(ramp_tasks=0)),
     ("gemm", dict(beta=1.0), dict(ramp_tasks=8, ramp_chunk_steps=1)),
+    ("gemm", dict(beta=1.0), dict(prefetch=0)),
+    ("syr2k", dict(uplo="lower", beta=1.0), dict(prefetch=0)),
+    ("syrk", dict(uplo="upper", trans_a=True, beta=0.5), dict(prefetch=1)),
+    ("symm", dict(uplo="lower", side="left", beta=1.0), dict(prefetch=1)),
 ])
 def test_launch_shape_options_on_hardware(kind, kw, opts):
     """The launch-shape knobs (chain split, KM split, substitution path with the reference's

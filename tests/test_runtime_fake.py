@@ -495,3 +495,63 @@ def test_split_km_trmm_matches_reference(case):
         for g in (o for o in prog.ops if type(o) is GemmOp):
             kms = {km != KM_NONE for _, _, _, km in g.subs}
             assert len(kms) == 1
+
+
+@pytest.mark.parametrize("kind", ["gemm", "syrk", "syr2k", "symm"])
+@pytest.mark.parametrize("prefetch", [-1, 0, 1])
+def test_small_call_prefetch(kind, prefetch, monkeypatch):
+    """RunOptions.prefetch: a small call on one GPU (resident issue engine) loads every
+    input tile at the start in first-use order; results, H2D bytes (each tile once) and
+    the task count are those of the unprefetched call."""
+    call = build_call(kind, m=96, n=80, k=72, tile_size=24, seed=4, beta=1.0, uplo="lower")
+    c0 = call.c.matrix.as_2d().copy()
+    eng = FakeEngine(1, seed=17, arena_bytes=1 << 24)
+    import paper_1510_05041_b200.scheduler as S
+    calls, inside = [], [False]
+    orig, real_prefetch = eng.ic_resolve, S._ic_prefetch
+
+    def spy(table, d, tids):
+        if inside[0]:
+            calls.append(list(tids))
+        return orig(table, d, tids)
+
+    def prefetch_spy(*a):
+        inside[0] = True
+        try:
+            real_prefetch(*a)
+        finally:
+            inside[0] = False
+    eng.ic_resolve = spy
+    monkeypatch.setattr(S, "_ic_prefetch", prefetch_spy)
+    topo1 = Topology([DeviceDesc(0)])
+    res = run_call(call, topo1, RunOptions(prefetch=prefetch), engine=eng)
+    out = call.c.matrix.as_2d().copy()
+    call.c.matrix.as_2d()[:] = c0
+    ref = run_call(call, topo1, RunOptions(prefetch=0), engine=FakeEngine(1, seed=3, arena_bytes=1 << 24))
+    np.testing.assert_allclose(out, call.c.matrix.as_2d(), rtol=1e-13, atol=1e-13)
+    assert res.metrics.total_h2d_bytes() == ref.metrics.total_h2d_bytes()
+    assert res.metrics.host_fetches == ref.metrics.host_fetches
+    n_inputs = len(res.plan.tasks[0]._bx_icgeom)
+    if prefetch != 0:                   # 1 and auto (this call has < 64 tasks)
+        assert calls and sorted(t for c in calls for t in c) == list(range(n_inputs))
+    else:
+        assert not calls
+
+
+def test_prefetch_only_on_one_gpu_and_small_calls():
+    from paper_1510_05041_b200.scheduler import SMALL_CALL_TASKS
+    call = build_call("gemm", m=96, n=80, k=72, tile_size=24, seed=4, beta=1.0)
+    eng = FakeEngine(2, seed=1, arena_bytes=1 << 24)
+    seen = []
+    orig = eng.ic_resolve
+    eng.ic_resolve = lambda *a: (seen.append(a), orig(*a))[1]
+    run_call(call, Topology([DeviceDesc(i, peer_group="g") for i in range(2)]), RunOptions(prefetch=1),
+             engine=eng)
+    assert not seen                                # two GPUs: no prefetch
+    big = build_call("gemm", m=8 * 24, n=8 * 24, k=48, tile_size=24, seed=2, beta=0.0)
+    eng1 = FakeEngine(1, seed=1, arena_bytes=1 << 24)
+    seen1 = []
+    orig1 = eng1.ic_resolve
+    eng1.ic_resolve = lambda *a: (seen1.append(a), orig1(*a))[1]
+    res = run_call(big, Topology([DeviceDesc(0)]), RunOptions(), engine=eng1)
+    assert len(res.plan.tasks) >= SMALL_CALL_TASKS and not seen1   # auto: large call, none
