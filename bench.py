@@ -439,6 +439,25 @@ def link_probe(eng, lib, slot, nbytes=256 << 20, reps=4, peers=None, sync_all=No
 
 # ----------------------------------------------------------------------------- the line
 
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_kernel_traffic_r02.json")
+
+
+def kernel_traffic(f32, shape):
+    """DRAM bytes (read + write) per launch of this exact kernel-leg launch (dtype and
+    m x n x k) from its committed ncu --set full capture (tools/kernel_traffic.py), or None
+    when no capture of this shape exists (a traffic figure is never borrowed from another
+    kernel or shape)."""
+    try:
+        tab = json.load(open(TRAFFIC_FILE))
+    except (OSError, ValueError):
+        return None, None
+    key = f"{'f32' if f32 else 'f64'} {'x'.join(str(int(x)) for x in shape)}"
+    ent = tab.get(key)
+    if not ent:
+        return None, None
+    return ent["traffic_bytes"], f"profiles/{os.path.basename(TRAFFIC_FILE)}[{key!r}] ({ent['source']})"
+
+
 def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parity,
                 execution="single process"):
     """The bench JSON line (shared by the single-process and one-process-per-GPU paths)."""
@@ -466,6 +485,8 @@ def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parit
             t_link += p2p_max / (links["p2p_in_gbs"] * 1e9) if links.get("p2p_in_gbs") else float("nan")
     t_meas = val["ms"] / 1e3
     roof = max(t_tensor, t_link or 0.0)
+    esz = 4 if f32 else 8
+    traffic, traffic_src = kernel_traffic(f32, kern["shape"])
     out = {
         "metric": METRIC_F32 if f32 else METRIC,
         "value": val["value"], "unit": "TFLOP/s",
@@ -486,7 +507,11 @@ def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parit
                   "per_device": val["per_device"]},
         "roofline": {"bound": "tensor", "achieved": kern["tflops"], "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": kern["tflops"] / peak_tf,
-                     "traffic": kern.get("traffic"),
+                     "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": esz * (kern["shape"][0] * kern["shape"][2]
+                                                            + kern["shape"][2] * kern["shape"][1]
+                                                            + (1 if f32 else 2) * kern["shape"][0] * kern["shape"][1]),
                      "kernel": ("bx::sgemm_tc2c_kernel (tcgen05.mma.cta_group::2 kind::tf32, 256x256 "
                                 "pair tiles taken by cluster launch control, double-buffered TMEM "
                                 "accumulators, TMA)" if f32 else
