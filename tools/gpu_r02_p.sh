@@ -12,4 +12,7 @@ timeout 900 $N -o $O/k_f32_32768 python tools/prof_kernel_leg.py 32768 32768 327
 python tools/kernel_traffic.py $O/ncu_kernel_traffic_r02.json $O/k_f64_2048.ncu-rep:f64:2048x2048x2048 \
   $O/k_f64_16384.ncu-rep:f64:16384x16384x16384 $O/k_f64_16384_8192.ncu-rep:f64:16384x16384x8192 \
   $O/k_f64_32768.ncu-rep:f64:32768x32768x32768 $O/k_f32_32768.ncu-rep:f32:32768x32768x32768 > $O/collect.log 2>&1
+
+for f in $O/k_*.ncu-rep; do python tools/ncu_summary.py $f > ${f%.ncu-rep}.txt 2>&1; done
+rm -f $O/k_f64_2048.ncu-rep $O/k_f64_16384_8192.ncu-rep $O/k_f64_32768.ncu-rep $O/k_f32_32768.ncu-rep $O/k_f64_16384.ncu-rep
 echo done > $O/status.txt

@@ -15,7 +15,8 @@ for spec in sys.argv[2:]:
     d = dict(zip(hdr, data))
     u = dict(zip(hdr, units))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-    tscale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+    tscale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
+              "s": 1e3, "second": 1e3}
     rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale[u["dram__bytes_read.sum"]]
     wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale[u["dram__bytes_write.sum"]]
     ms = float(d["gpu__time_duration.sum"].replace(",", "")) * tscale[u["gpu__time_duration.sum"]]
