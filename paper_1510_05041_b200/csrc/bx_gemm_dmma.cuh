@@ -203,23 +203,34 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_task_kernel(const __grid
   cp_async_wait<0>();
 
   // epilogue: C = alpha*acc + beta*C  (beta == 0: C never read)
+  // epilogue, one fragment row i at a time: with beta != 0 its NF x 2 C loads are all
+  // issued before the first store (one memory round trip per row instead of 2 NF
+  // dependent ones — the epilogue of a short launch with beta = 1 is otherwise a few % of it)
   const double alpha = t.alpha, beta = t.beta;
 #pragma unroll
   for (int i = 0; i < MF; ++i) {
     const int r = m0 + wm + i * 8 + g;
     if (r >= t.h) continue;
+    double cv[NF][2];
+    bool ok[NF][2];
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = n0 + wn + j * 8 + 2 * q + e;
-        if (cc >= t.w) continue;
-        if (t.tri == TRI_LOWER && cc > r) continue;
-        if (t.tri == TRI_UPPER && cc < r) continue;
-        double* p = t.c + (size_t)cc * t.ldc + r;
+        ok[j][e] = cc < t.w && !(t.tri == TRI_LOWER && cc > r) && !(t.tri == TRI_UPPER && cc < r);
+        cv[j][e] = (beta != 0.0 && ok[j][e]) ? t.c[(size_t)cc * t.ldc + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!ok[j][e]) continue;
+        const int cc = n0 + wn + j * 8 + 2 * q + e;
         double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v = fma(beta, *p, v);
-        *p = v;
+        if (beta != 0.0) v = fma(beta, cv[j][e], v);
+        t.c[(size_t)cc * t.ldc + r] = v;
       }
     }
   }
@@ -462,23 +473,34 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS) gemm_task_mb_ke
   }
   cp_async_wait<0>();
 
+  // epilogue, one fragment row i at a time: with beta != 0 its NF x 2 C loads are all
+  // issued before the first store (one memory round trip per row instead of 2 NF
+  // dependent ones — the epilogue of a short launch with beta = 1 is otherwise a few % of it)
   const double alpha = t.alpha, beta = t.beta;
 #pragma unroll
   for (int i = 0; i < MF; ++i) {
     const int r = m0 + wm + i * 8 + g;
     if (r >= t.h) continue;
+    double cv[NF][2];
+    bool ok[NF][2];
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = n0 + wn + j * 8 + 2 * q + e;
-        if (cc >= t.w) continue;
-        if (t.tri == TRI_LOWER && cc > r) continue;
-        if (t.tri == TRI_UPPER && cc < r) continue;
-        double* p = t.c + (size_t)cc * t.ldc + r;
+        ok[j][e] = cc < t.w && !(t.tri == TRI_LOWER && cc > r) && !(t.tri == TRI_UPPER && cc < r);
+        cv[j][e] = (beta != 0.0 && ok[j][e]) ? t.c[(size_t)cc * t.ldc + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!ok[j][e]) continue;
+        const int cc = n0 + wn + j * 8 + 2 * q + e;
         double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v = fma(beta, *p, v);
-        *p = v;
+        if (beta != 0.0) v = fma(beta, cv[j][e], v);
+        t.c[(size_t)cc * t.ldc + r] = v;
       }
     }
   }
@@ -657,23 +679,34 @@ __global__ void __launch_bounds__(T_THREADS_G, 1) gemm_task_tma_kernel(const __g
     }
   }
 
+  // epilogue, one fragment row i at a time: with beta != 0 its NF x 2 C loads are all
+  // issued before the first store (one memory round trip per row instead of 2 NF
+  // dependent ones — the epilogue of a short launch with beta = 1 is otherwise a few % of it)
   const double alpha = t.alpha, beta = t.beta;
 #pragma unroll
   for (int i = 0; i < MF; ++i) {
     const int r = m0 + wm + i * 8 + g;
     if (r >= t.h) continue;
+    double cv[NF][2];
+    bool ok[NF][2];
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = n0 + wn + j * 8 + 2 * q + e;
-        if (cc >= t.w) continue;
-        if (t.tri == TRI_LOWER && cc > r) continue;
-        if (t.tri == TRI_UPPER && cc < r) continue;
-        double* p = t.c + (size_t)cc * t.ldc + r;
+        ok[j][e] = cc < t.w && !(t.tri == TRI_LOWER && cc > r) && !(t.tri == TRI_UPPER && cc < r);
+        cv[j][e] = (beta != 0.0 && ok[j][e]) ? t.c[(size_t)cc * t.ldc + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!ok[j][e]) continue;
+        const int cc = n0 + wn + j * 8 + 2 * q + e;
         double v = alpha * acc[i][j][e];
-        if (beta != 0.0) v = fma(beta, *p, v);
-        *p = v;
+        if (beta != 0.0) v = fma(beta, cv[j][e], v);
+        t.c[(size_t)cc * t.ldc + r] = v;
       }
     }
   }

@@ -78,6 +78,28 @@ __device__ __forceinline__ void s_tma_3d(void* dst, const CUtensorMap* map, uint
 __device__ __forceinline__ void s_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void s_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
+// Epilogue: 16 consecutive columns of one output row (lane = row, so each store
+// instruction of a warp writes 32 consecutive floats).  With beta != 0 the 16 C loads are
+// all issued before the first store: one memory round trip per 16 columns instead of 16
+// dependent ones (which made a beta = 1 epilogue longer than the mainloop of a K = 8192
+// pair tile).
+__device__ __forceinline__ void s_store16(const SgemmTask& t, const uint32_t* v, int row, int col0) {
+  float* base = t.c + (size_t)col0 * t.ldc + row;
+  float cv[16];
+  if (t.beta != 0.0f) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cv[i] = col0 + i < t.w ? base[(size_t)i * t.ldc] : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (col0 + i < t.w) {
+      float r = t.alpha * __uint_as_float(v[i]);
+      if (t.beta != 0.0f) r = fmaf(t.beta, cv[i], r);
+      base[(size_t)i * t.ldc] = r;
+    }
+  }
+}
+
 // shared-memory matrix descriptor (sm100 "version 1").  layout 2 = SWIZZLE_128B (K-major
 // operands, 8 rows x 128 B atoms); layout 1 = SWIZZLE_128B_BASE32B (32-bit MN-major
 // operands: 4 k-rows x 128 B atoms, 32-B swizzle granules — TMA's SWIZZLE_128B_ATOM_32B).
@@ -259,16 +281,7 @@ __global__ void __launch_bounds__(S_THREADS, 1) sgemm_tc_kernel(const __grid_con
         for (int i = 0; i < 16; ++i) v[i] = 0u;
       }
       if (row < t.h && !(t.dbg & 8)) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = n0 + c0 + i;
-          if (col < t.w) {
-            float* p = t.c + (size_t)col * t.ldc + row;
-            float r = t.alpha * __uint_as_float(v[i]);
-            if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
-            *p = r;
-          }
-        }
+        s_store16(t, v, row, n0 + c0);
       }
     }
   }
@@ -468,16 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         for (int i = 0; i < 16; ++i) v[i] = 0u;
       }
       if (row < t.h) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = n0 + c0 + i;
-          if (col < t.w) {
-            float* p = t.c + (size_t)col * t.ldc + row;
-            float r = t.alpha * __uint_as_float(v[i]);
-            if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
-            *p = r;
-          }
-        }
+        s_store16(t, v, row, n0 + c0);
       }
     }
   }
@@ -668,16 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           if (lane == 0) p_arrive_cluster(lead_tempty[b]);
         }
         if (row < t.h) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = n0 + c0 + i;
-            if (col < t.w) {
-              float* p = t.c + (size_t)col * t.ldc + row;
-              float r = t.alpha * __uint_as_float(v[i]);
-              if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
-              *p = r;
-            }
-          }
+          s_store16(t, v, row, n0 + c0);
         }
       }
     }
@@ -930,16 +925,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           if (lane == 0) p_arrive_cluster(lead_tempty[b]);
         }
         if (row < t.h) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = n0 + c0 + i;
-            if (col < t.w) {
-              float* p = t.c + (size_t)col * t.ldc + row;
-              float r = t.alpha * __uint_as_float(v[i]);
-              if (t.beta != 0.0f) r = fmaf(t.beta, *p, r);
-              *p = r;
-            }
-          }
+          s_store16(t, v, row, n0 + c0);
         }
       }
       // next tile: every lane reads the response, one arrival per warp
