@@ -1471,10 +1471,10 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
     _ic_setup(plan, options, workers, engine, topology)
     for w in workers:
         w.epoch = engine.record(w.slot, 0, timing=True)
-    _ic_prefetch(plan, options, workers, engine)
     t0 = time.perf_counter()
     t_setup = t0 - t_setup0
     try:
+        _ic_prefetch(plan, options, workers, engine)
         if options.execution == "deterministic":
             _drive_single(rt, workers)
         else:
