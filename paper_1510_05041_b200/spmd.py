@@ -171,6 +171,9 @@ class Session:
         self._shm = []
         self._peer = {}              # rank -> (arena gen, base)
         self._arena_gen = 0
+        self._seq = 0                # calls made (every rank calls in the same order)
+        self._nshare = 0             # share_call invocations
+        self._blocks = [None, None]  # pooled call files, by call parity: (ShmFile, mapped dptr)
         self.barrier("session start")
 
     # ---- coordination ----------------------------------------------------------------
@@ -209,8 +212,31 @@ class Session:
         return out
 
     def next_call(self) -> int:
-        """All ranks advance the call sequence together (called between barriers)."""
-        return int(self.hdr[2]) + 1
+        """All ranks advance the call sequence together (collective: every rank makes the
+        same calls in the same order)."""
+        self._seq += 1
+        return self._seq
+
+    def call_file(self, eng, seq: int, nbytes: int):
+        """The pooled node-shared file for call ``seq`` (calls alternate between two, so a
+        file is reused only after every rank has started the following call, i.e. finished
+        reading this one), at least ``nbytes`` long, page-locked and mapped for the GPU.
+        Returns (ShmFile, device address of its first byte).  Collective."""
+        par = seq & 1
+        have = self._blocks[par]
+        if have is not None and have[0].nbytes >= nbytes:
+            return have
+        if have is not None:              # too small: last used two calls ago
+            try:
+                eng.unregister_host(have[0].buf)
+            except Exception:
+                pass
+            if self.rank == 0:
+                have[0].unlink()
+        size = max(nbytes, 2 * have[0].nbytes if have is not None else 0)
+        f = ShmFile(f"bx_{self.job}_callblk{par}_{seq}", size, create=self.rank == 0)
+        self._blocks[par] = (f, eng.register_mapped(f.buf))
+        return self._blocks[par]
 
     # ---- node-shared host memory -----------------------------------------------------
 
@@ -255,10 +281,10 @@ class Session:
             f = ShmFile(f"bx_{self.job}_callmeta", 1 << 16, create=False)
             n = int(f.view(0, 1, np.int64)[0])
             meta = json.loads(bytes(f.view(8, n, np.uint8)).decode())
-        seq = int(self.hdr[2])
+        self._nshare += 1
         tiled = {}
         for k, d in meta["ops"].items():
-            arr = self.shared_array(f"{seq}_{k}_{d['id']}", d["n"], np.dtype(d["dtype"]))
+            arr = self.shared_array(f"share{self._nshare}_{k}_{d['id']}", d["n"], np.dtype(d["dtype"]))
             if self.rank == 0:
                 arr[:] = getattr(call, k).matrix.storage
             tiled[k] = make_tiled(MatrixDesc(d["id"], d["rows"], d["cols"], d["ld"], arr, d["base"]),
@@ -300,7 +326,7 @@ class Session:
         return out
 
     def close(self) -> None:
-        for f in self._shm:
+        for f in self._shm + [b[0] for b in self._blocks if b is not None]:
             if self.rank == 0:
                 f.unlink()
         if self.rank == 0:
@@ -349,11 +375,14 @@ class _CallBlock:
     """Shared state of one call.  int64 regions: header (0 queue head, 1 queue tail,
     2 tasks done), queue, dependency counters, station slots + published priorities, first
     holder per tile, arena offset per (tile, rank); float64 metrics per rank; uint32 arrival
-    flags per (tile, rank) (page-aligned: mapped for the GPU's stream memory operations)."""
+    flags per (tile, rank) (page-aligned: mapped for the GPU's stream memory operations).
 
-    def __init__(self, sess: Session, seq: int, n_tasks: int, n_tiles: int, create: bool):
-        W = sess.world
-        self.W = W
+    The views lie over a pooled node-shared file (``Session.call_file``): a session keeps
+    two, used by alternate calls, page-locked and mapped for the GPU once, so a call pays
+    neither the file creation nor the registration (≈ 3 ms per call per rank)."""
+
+    @staticmethod
+    def layout(W: int, n_tasks: int, n_tiles: int):
         sizes = [("hdr", 8), ("queue", n_tasks), ("deps", n_tasks), ("rs", W * RS_SLOTS),
                  ("rsprio", W * RS_SLOTS), ("owner", n_tiles), ("offs", n_tiles * W),
                  ("met", W * (MET_FIELDS + W))]
@@ -364,13 +393,23 @@ class _CallBlock:
             off += 8 * n
         flags_off = (off + 4095) // 4096 * 4096
         total = flags_off + max(4096, (4 * n_tiles * W + 4095) // 4096 * 4096)
-        self.file = ShmFile(f"bx_{sess.job}_call{seq}", total, create=create)
+        return lay, flags_off, total
+
+    def __init__(self, sess: Session, file: "ShmFile", n_tasks: int, n_tiles: int):
+        W = sess.world
+        self.W = W
+        lay, self.flags_off, self.total = self.layout(W, n_tasks, n_tiles)
+        self.file = file
         for name, (o, n) in lay.items():
             setattr(self, name, self.file.view(o, n, np.float64 if name == "met" else np.int64))
-        self.flags = self.file.view(flags_off, n_tiles * W, np.uint32)
+        self.flags = self.file.view(self.flags_off, n_tiles * W, np.uint32)
         self.rs2 = self.rs.reshape(W, RS_SLOTS)
         self.rsprio2 = self.rsprio.reshape(W, RS_SLOTS)
         self.met2 = self.met.reshape(W, MET_FIELDS + W)
+
+    def clear(self) -> None:
+        """Zero this call's regions (rank 0, before the block is published)."""
+        self.file.buf[:self.total] = 0
 
     # ---- shared FIFO ----
     def push(self, task_id: int) -> None:
@@ -725,9 +764,11 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
 
     tbase, n_tiles = _tile_index(plan)
     n_tasks = len(plan.tasks)
-    blk = None
+    _lay, flags_off, total = _CallBlock.layout(W, n_tasks, n_tiles)
+    cfile, base_dptr = sess.call_file(engine, seq, total)
+    blk = _CallBlock(sess, cfile, n_tasks, n_tiles)
     if r == 0:
-        blk = _CallBlock(sess, seq, n_tasks, n_tiles, create=True)
+        blk.clear()
         tail = 0
         for t in plan.tasks:
             blk.deps[t.task_id] = t.deps_remaining
@@ -736,9 +777,7 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
                 tail += 1
         blk.hdr[1] = tail
     sess.barrier("call block created")
-    if r != 0:
-        blk = _CallBlock(sess, seq, n_tasks, n_tiles, create=False)
-    flags_dptr = engine.register_mapped(blk.flags)
+    flags_dptr = base_dptr + flags_off
     bases = sess.peer_bases(engine, slot)
     topo = Topology([DeviceDesc(q, peer_group="spmd") for q in range(W)])
     rt = SpmdRuntime(plan, topo, options, engine, sess, blk)
@@ -787,20 +826,17 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
             engine.unregister_host(p)
         except Exception:
             pass
-    try:
-        engine.unregister_host(blk.flags)
-    except Exception:
-        pass
     metrics = None
     if not failed:
+        # the block is reused two calls later, after every rank has passed the next call's
+        # "call block created" barrier, i.e. after this read
         metrics = _gather_metrics(plan, blk, W, wall)
-    sess.barrier("call results read")
-    if r == 0:
-        blk.file.unlink()
-        sess.hdr[2] = seq
-        sess.hdr[5] = 0
-        sess.hdr[6] = 0
-    sess.barrier("call closed")
+    else:
+        sess.barrier("call results read")
+        if r == 0:
+            sess.hdr[5] = 0
+            sess.hdr[6] = 0
+        sess.barrier("call closed")
     if snap_shm is not None:
         try:
             engine.unregister_host(arr)

@@ -83,9 +83,11 @@ class SpmdFakeEngine(FakeEngine):
         self._remote.pop(base, None)
 
     def register_mapped(self, array):
+        # any page-locked host range (the runtime maps a whole call file); flags are the
+        # uint32 words at dptr offsets from its base
         base = (1 << 56) + (self._next_tok << 40)
         self._next_tok += 1
-        self._mapped[base] = array
+        self._mapped[base] = array.view(np.uint8).reshape(-1)
         return base
 
     def unregister_host(self, array):
@@ -97,8 +99,9 @@ class SpmdFakeEngine(FakeEngine):
 
     def _flag(self, dptr):
         for b, a in self._mapped.items():
-            if b <= dptr < b + 4 * a.size:
-                return a, (dptr - b) // 4
+            if b <= dptr < b + a.nbytes:
+                assert (dptr - b) % 4 == 0, "misaligned flag"
+                return a[:a.nbytes // 4 * 4].view(np.uint32), (dptr - b) // 4
         raise AssertionError(f"unmapped flag address {dptr:#x}")
 
     def copy_remote(self, slot, dst_off, src_ptr, nbytes, flag_dptr=0, flag_min=0, waits=()):

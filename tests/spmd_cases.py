@@ -132,3 +132,31 @@ def run_steal_stress(n, tile, calls, rs_capacity):
     finally:
         eng.cleanup()
     return out
+
+
+def run_size_sequence(sizes, tile, fake):
+    """Every rank: one session, calls of alternating sizes (the pooled call files are reused
+    by alternate calls and grown when a larger call comes); rank 0 checks each result.
+    Returns, per call, (tasks this rank ran, tasks in the plan, rank 0's max error)."""
+    from paper_1510_05041_b200 import RunOptions, build_call, run_call, spmd
+    sess = spmd.init()
+    eng = None
+    if fake:
+        from fake_spmd import SpmdFakeEngine
+        eng = SpmdFakeEngine(sess.rank, sess.job, seed=sess.rank * 13 + 5)
+    out = []
+    try:
+        for i, n in enumerate(sizes):
+            call = ref = None
+            if sess.rank == 0:
+                call = build_call("gemm", m=n, n=n, k=n // 2, tile_size=tile, seed=i, alpha=1.0,
+                                  beta=1.0)
+                ref = _reference(call)
+            call = sess.share_call(call)
+            res = run_call(call, options=RunOptions(execution="spmd"), engine=eng)
+            err = float(np.max(np.abs(call.c.matrix.as_2d() - ref))) if sess.rank == 0 else 0.0
+            out.append((res.tasks_by_device[sess.rank], len(res.plan.tasks), err))
+        return out
+    finally:
+        if eng is not None:
+            eng.cleanup()

@@ -7,6 +7,7 @@ checks nothing itself; rank 0 compares the shared output with the oracle).  GPU:
 cases with the real engine, several ranks sharing GPU 0 (IPC + stream memory operations on
 hardware)."""
 
+import os
 import pytest
 
 import spmd_cases as SC
@@ -104,3 +105,48 @@ def test_spmd_station_stealing_stress():
     for c in range(3):
         assert sum(o[c][0] for o in outs) == outs[0][c][1], [o[c] for o in outs]
         assert outs[0][c][2] <= 1e-11, outs[0][c]
+
+
+def test_spmd_pooled_call_files_reuse_and_growth():
+    """Calls alternate between two pooled node-shared call files: small, large (grows one
+    file), small, large, larger (grows the other) — every call still runs every task once
+    and matches the reference."""
+    sizes = [64, 256, 64, 256, 320, 64]
+    outs = spmd.launch(2, SC.run_size_sequence, sizes, 32, True, timeout=600)
+    for c in range(len(sizes)):
+        assert sum(o[c][0] for o in outs) == outs[0][c][1], [o[c] for o in outs]
+        assert outs[0][c][2] <= 1e-11 * 64, outs[0][c]
+
+
+def test_call_file_pool_growth_is_collective():
+    """Session.call_file: alternate calls use two files; a file is replaced (unregistered,
+    unlinked by rank 0) only when a call needs more bytes, and the replacement at least
+    doubles it."""
+
+    class Eng:
+        def __init__(self):
+            self.mapped, self.unmapped = [], []
+
+        def register_mapped(self, a):
+            self.mapped.append(a.nbytes)
+            return 1 << 40
+
+        def unregister_host(self, a):
+            self.unmapped.append(a.nbytes)
+
+    sess = spmd.Session.__new__(spmd.Session)
+    sess.rank, sess.job, sess._blocks = 0, f"t{os.getpid()}", [None, None]
+    eng = Eng()
+    try:
+        f1, _ = sess.call_file(eng, 1, 5000)
+        f2, _ = sess.call_file(eng, 2, 5000)
+        assert f1 is not f2 and eng.mapped == [5000, 5000]
+        assert sess.call_file(eng, 3, 4000)[0] is f1          # reused: big enough
+        f5, _ = sess.call_file(eng, 5, 6000)                    # parity 1 grows
+        assert f5 is not f1 and f5.nbytes >= 10000 and eng.unmapped == [5000]
+        assert not os.path.exists(f1.path)
+        assert sess.call_file(eng, 4, 5000)[0] is f2
+    finally:
+        for b in sess._blocks:
+            if b is not None:
+                b[0].unlink()
