@@ -348,9 +348,11 @@ def init(rank: Optional[int] = None, world: Optional[int] = None, device: Option
     world = int(env.get("WORLD_SIZE", 1)) if world is None else world
     device = int(env.get("LOCAL_RANK", rank)) if device is None else device
     if job is None:
-        job = env.get("BX_SPMD_JOB") or env.get("TORCHELASTIC_RUN_ID") or env.get("MASTER_PORT")
+        job = env.get("BX_SPMD_JOB") or env.get("TORCHELASTIC_RUN_ID")
         if not job or job == "none":
-            job = f"p{env.get('MASTER_PORT', '0')}"
+            # torchrun without an rdzv id: the ranks of one launch share the agent process
+            # (their parent), so a rerun on the same port never joins a stale session file
+            job = f"p{env.get('MASTER_PORT', '0')}_{os.getppid()}"
     job = "".join(ch if ch.isalnum() else "_" for ch in str(job))
     _SESSION = Session(rank, world, device, job)
     return _SESSION
