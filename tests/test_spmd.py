@@ -150,3 +150,22 @@ def test_call_file_pool_growth_is_collective():
         for b in sess._blocks:
             if b is not None:
                 b[0].unlink()
+
+
+def test_torchrun_job_name_is_launch_unique(monkeypatch):
+    """torchrun without an rdzv id exports TORCHELASTIC_RUN_ID=none: the session name then
+    carries the port and the agent's pid (every rank's parent), so two launches on one port
+    never share session files."""
+    for k in ("BX_SPMD_JOB",):
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("TORCHELASTIC_RUN_ID", "none")
+    monkeypatch.setenv("MASTER_PORT", "29577")
+    monkeypatch.setenv("RANK", "0")
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setenv("LOCAL_RANK", "0")
+    monkeypatch.setattr(spmd, "_SESSION", None)
+    sess = spmd.init()
+    try:
+        assert sess.job == f"p29577_{os.getppid()}"
+    finally:
+        spmd.shutdown()
