@@ -173,6 +173,15 @@ def tf32_peak_tflops():
         return 1590.0 / 2.0, "fallback 1.59 PF bf16 / 2 (B200_PROFILING.md)"
 
 
+def tf32_sustained_tflops():
+    """Half of MEASURED_PEAKS.json's sustained (back-to-back, power-capped) bf16 rate, or None."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return mp["bf16_tflops_sustained"] / 2.0
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def config_dict(cfg, args):
     """The ``config`` object — identical for both arms (same routine, shape and scalars)."""
     return {"workload": cfg["desc"], "routine": cfg["kind"], "m": cfg["m"], "n": cfg["n"],
@@ -507,6 +516,8 @@ def result_line(args, cfg, val, e2e, kern, peak_measured, clk, cpu, links, parit
                   "per_device": val["per_device"]},
         "roofline": {"bound": "tensor", "achieved": kern["tflops"], "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": kern["tflops"] / peak_tf,
+                     "frac_of_sustained_peak": (kern["tflops"] / tf32_sustained_tflops()
+                                                if f32 and tf32_sustained_tflops() else None),
                      "traffic": traffic,
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": esz * (kern["shape"][0] * kern["shape"][2]
