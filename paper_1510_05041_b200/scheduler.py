@@ -1332,7 +1332,8 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
     return max(min(want, cap), (WORKING_SET_TILES + 1) * per_tile)
 
 
-def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOptions:
+def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int,
+                    bounded_arena: bool = False) -> RunOptions:
     """Auto launch shape.  chunk_steps=0: 8 k-steps per launch for GEMM/SYMM/SYR2K, 16
     otherwise (SYR2K 137.2 -> 130.3 ms; TRMM better at 16).
     n_streams=0: 4 compute streams (the reference's lanes, devices.py:36); GEMM/SYMM, TRSM
@@ -1349,6 +1350,11 @@ def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunO
         options = dataclasses.replace(options, chunk_steps=8 if kind in ("gemm", "symm", "syr2k") else 16)
     if options.n_streams:
         return options
+    if n_devices == 1 and 0 < len(plan.tasks) < SMALL_CALL_TASKS and not bounded_arena:
+        # a small call on one GPU (auto-sized arena) has nothing to balance: one task per
+        # stream, up to 16 (cfg1, 16 tasks: 2.7 -> 2.6 ms against the capped 4 streams,
+        # profiles/small_call_ab_r02.txt)
+        return dataclasses.replace(options, n_streams=min(16, len(plan.tasks)))
     want = {"trsm": 8, "trmm": 8, "syrk": 12, "gemm": 8, "symm": 8}.get(kind, 4)
     share = len(plan.tasks) // max(1, n_devices)
     cap = max(4, share // (4 * max(1, options.tasks_per_stream)))
@@ -1403,7 +1409,8 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
         return spmd.run_plan_spmd(plan, options, engine, _t_plan=_t_plan)
     topology = topology or discover_topology()
     devs = topology.accelerators()
-    options = resolve_streams(plan, options, len(devs))
+    bounded = bool(options.arena_bytes) or any(d.arena_capacity for d in devs)
+    options = resolve_streams(plan, options, len(devs), bounded)
     options = resolve_ramp(plan, options, len(devs))
     if engine is None:
         engine = get_engine([d.device_id for d in devs], options.n_streams,

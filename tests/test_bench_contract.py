@@ -119,3 +119,16 @@ def test_no_start_up_batch_for_small_calls():
     assert len(plan.tasks) == 16
     assert resolve_ramp(plan, RunOptions(), 1).ramp_tasks == 0
     assert resolve_ramp(plan, RunOptions(ramp_tasks=4), 1).ramp_tasks == 4
+
+
+def test_small_call_one_stream_per_task():
+    """Small calls (< 64 tasks) on one GPU with an auto-sized arena: one task per compute
+    stream (up to 16); bounded arenas and several GPUs keep the capped default."""
+    call = build_call("gemm", m=256, n=256, k=256, tile_size=64, seed=0, beta=1.0)
+    plan = generate_tasks(call)
+    assert resolve_streams(plan, RunOptions(), 1).n_streams == 16
+    assert resolve_streams(plan, RunOptions(), 1, bounded_arena=True).n_streams == 4
+    assert resolve_streams(plan, RunOptions(), 2).n_streams == 4
+    assert resolve_streams(plan, RunOptions(n_streams=3), 1).n_streams == 3
+    tiny = generate_tasks(build_call("gemm", m=128, n=64, k=64, tile_size=64, seed=0))
+    assert resolve_streams(tiny, RunOptions(), 1).n_streams == len(tiny.tasks) == 2
