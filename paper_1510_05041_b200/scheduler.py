@@ -37,14 +37,13 @@ from typing import Optional
 
 import numpy as np
 
-from .cache import HOST_FETCH, L1_HIT, L2_HIT, CoherenceDirectory, DeviceTileCache, LruBlock
+from .cache import HOST_FETCH, L2_HIT, CoherenceDirectory, DeviceTileCache, LruBlock
 from .devices import (DeviceMetrics, Metrics, Topology, TraceEvent, discover_topology,
                       exposed_comm_time)
 from .errors import (ArenaOutOfMemoryError, CapacityDeadlockError, ConfigError,
                      SingularMatrixError)
 from .memory import Arena
-from .routines import (GEMM_UPDATE, SYMM_DIAG, SYR2K_UPDATE, SYRK_UPDATE, TRMM_DIAG,
-                       TRSM_SOLVE, RoutineCall, Task, TaskPlan, generate_tasks)
+from .routines import RoutineCall, Task, TaskPlan, generate_tasks
 from .program import AxpyOp, GemmOp, MatOp, TrsmOp, compile_task, scratch_key
 from .tiling import device_ld
 
