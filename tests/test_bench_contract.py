@@ -132,3 +132,24 @@ def test_small_call_one_stream_per_task():
     assert resolve_streams(plan, RunOptions(n_streams=3), 1).n_streams == 3
     tiny = generate_tasks(build_call("gemm", m=128, n=64, k=64, tile_size=64, seed=0))
     assert resolve_streams(tiny, RunOptions(), 1).n_streams == len(tiny.tasks) == 2
+
+
+@pytest.mark.gpu
+def test_bench_runs_end_to_end_on_the_gpu():
+    """The driver's command shape on a B200 (small config, one step): one JSON line with the
+    contract keys, the parity check passing, kernels launched, the traffic field sourced."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "cfg1",
+                          "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    for k in REQUIRED + ["parity", "cache"]:
+        assert k in d, k
+    assert d["parity"]["pass"] and d["parity"]["max_ratio"] <= 10
+    assert d["gpu_launches"] > 0 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["roofline"]["traffic"] and "ncu_kernel_traffic" in d["roofline"]["traffic_source"]
+    assert d["warmup"] >= 3
