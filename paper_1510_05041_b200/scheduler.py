@@ -118,7 +118,7 @@ class RunOptions:
                                        # computed once per diagonal tile; 0 = substitution
     prefetch: int = -1                 # 1: load every input tile at the call's start in
                                        # first-use order (one GPU, resident issue engine);
-                                       # -1 = auto (calls of < SMALL_CALL_TASKS tasks), 0 off
+                                       # -1 = auto (scheduler.small_call), 0 off
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 
@@ -1261,11 +1261,31 @@ def _ic_setup(plan, options, workers, engine, topology) -> None:
 
 
 SMALL_CALL_TASKS = 64    # below this a call has no start-up batch and may prefetch
+LINK_BOUND_CALL_TASKS = 128   # ... and up to this many if its host traffic outlasts its math
+
+
+def small_call(plan: TaskPlan, n_devices: int = 1) -> bool:
+    """A call whose tasks can all be in flight at once: fewer than SMALL_CALL_TASKS, or up
+    to LINK_BOUND_CALL_TASKS when it is host-link bound (its operand bytes at the ~54 GB/s
+    of one host link take longer than its flops at the tensor rate: DGEMM 4096^3 at T=512,
+    64 tasks, 11.0 -> 10.1 ms with the small-call rules; DGEMM 8192^3 at T=1024, 64 tasks
+    but balanced, is better without them, profiles/small_call_ab_r02.txt)."""
+    n = len(plan.tasks)
+    if n < SMALL_CALL_TASKS:
+        return True
+    if n > LINK_BOUND_CALL_TASKS or n_devices > 1:
+        return False
+    esz = plan.dtype.itemsize
+    call = plan.call
+    nbytes = sum(m.rows * m.cols * esz for m in (call.a.matrix, call.b.matrix if call.b else None,
+                                                   call.c.matrix) if m is not None)
+    t_link = nbytes / 54e9
+    t_math = plan.total_flops / (35e12 if esz == 8 else 600e12)
+    return t_link > 1.5 * t_math
 
 
 def _ic_prefetch(plan, options, workers, engine) -> None:
-    """Small calls on one GPU (RunOptions.prefetch, auto: fewer than SMALL_CALL_TASKS
-    tasks): enqueue every input tile's host load at the start, in the order the tasks will
+    """Small calls on one GPU (RunOptions.prefetch, auto: ``small_call``): enqueue every input tile's host load at the start, in the order the tasks will
     first read them (FIFO task order, then step order), one arrival event per task's new
     tiles.  The H2D lane then streams back to back instead of following the host's task
     issue rate; launches find the tiles present (or in flight: they wait on the arrival
@@ -1274,7 +1294,7 @@ def _ic_prefetch(plan, options, workers, engine) -> None:
     C tiles would queue behind the whole prefetch on the one H2D lane."""
     want = options.prefetch
     if want < 0:
-        want = len(plan.tasks) < SMALL_CALL_TASKS
+        want = small_call(plan)
     if not want or len(workers) != 1 or workers[0].ic is None:
         return
     w = workers[0]
@@ -1349,7 +1369,7 @@ def resolve_streams(plan: TaskPlan, options: RunOptions, n_devices: int,
         options = dataclasses.replace(options, chunk_steps=8 if kind in ("gemm", "symm", "syr2k") else 16)
     if options.n_streams:
         return options
-    if n_devices == 1 and 0 < len(plan.tasks) < SMALL_CALL_TASKS and not bounded_arena:
+    if n_devices == 1 and plan.tasks and small_call(plan) and not bounded_arena:
         # a small call on one GPU (auto-sized arena) has nothing to balance: one task per
         # stream, up to 16 (cfg1, 16 tasks: 2.7 -> 2.6 ms against the capped 4 streams,
         # profiles/small_call_ab_r02.txt)
@@ -1370,7 +1390,7 @@ def resolve_ramp(plan: TaskPlan, options: RunOptions, n_devices: int) -> RunOpti
         return options
     import dataclasses
     ntasks = len(plan.tasks)
-    ramp = min(32, ntasks // (4 * max(1, n_devices))) if ntasks >= SMALL_CALL_TASKS else 0
+    ramp = min(32, ntasks // (4 * max(1, n_devices))) if not small_call(plan, n_devices) else 0
     return dataclasses.replace(options, ramp_tasks=ramp if ramp >= 4 else 0)
 
 

@@ -153,3 +153,26 @@ def test_bench_runs_end_to_end_on_the_gpu():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["roofline"]["traffic"] and "ncu_kernel_traffic" in d["roofline"]["traffic_source"]
     assert d["warmup"] >= 3
+
+
+def test_small_call_rule_counts_link_bound_mid_size_calls():
+    """64-128 tasks count as small on one GPU only when host-link bound: DGEMM 4096^3 at
+    T=512 (64 tasks, 0.38 GB for 0.14 TFLOP) yes, 8192^3 at T=1024 (64 tasks, balanced) no."""
+    from paper_1510_05041_b200.scheduler import small_call
+    from paper_1510_05041_b200 import RoutineCall
+    from paper_1510_05041_b200.tiling import MatrixDesc, make_tiled
+    import numpy as np
+
+    def plan_of(n, t):
+        buf = np.zeros(n * n)      # one buffer for all three operands: only geometry matters
+        return generate_tasks(RoutineCall("gemm", a=make_tiled(MatrixDesc("A", n, n, n, buf), t),
+                                          b=make_tiled(MatrixDesc("B", n, n, n, buf), t),
+                                          c=make_tiled(MatrixDesc("C", n, n, n, buf), t), beta=1.0))
+    p1 = plan_of(4096, 512)
+    p2 = plan_of(8192, 1024)
+    assert len(p1.tasks) == len(p2.tasks) == 64
+    assert small_call(p1) and not small_call(p2)
+    assert not small_call(p1, n_devices=2)
+    assert resolve_ramp(p1, RunOptions(), 1).ramp_tasks == 0
+    assert resolve_ramp(p2, RunOptions(), 1).ramp_tasks == 16
+    assert resolve_streams(p1, RunOptions(), 1).n_streams == 16

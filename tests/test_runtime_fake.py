@@ -539,7 +539,7 @@ def test_small_call_prefetch(kind, prefetch, monkeypatch):
 
 
 def test_prefetch_only_on_one_gpu_and_small_calls():
-    from paper_1510_05041_b200.scheduler import SMALL_CALL_TASKS
+    from paper_1510_05041_b200.scheduler import LINK_BOUND_CALL_TASKS
     call = build_call("gemm", m=96, n=80, k=72, tile_size=24, seed=4, beta=1.0)
     eng = FakeEngine(2, seed=1, arena_bytes=1 << 24)
     seen = []
@@ -548,10 +548,10 @@ def test_prefetch_only_on_one_gpu_and_small_calls():
     run_call(call, Topology([DeviceDesc(i, peer_group="g") for i in range(2)]), RunOptions(prefetch=1),
              engine=eng)
     assert not seen                                # two GPUs: no prefetch
-    big = build_call("gemm", m=8 * 24, n=8 * 24, k=48, tile_size=24, seed=2, beta=0.0)
+    big = build_call("gemm", m=12 * 24, n=12 * 24, k=48, tile_size=24, seed=2, beta=0.0)
     eng1 = FakeEngine(1, seed=1, arena_bytes=1 << 24)
     seen1 = []
     orig1 = eng1.ic_resolve
     eng1.ic_resolve = lambda *a: (seen1.append(a), orig1(*a))[1]
     res = run_call(big, Topology([DeviceDesc(0)]), RunOptions(), engine=eng1)
-    assert len(res.plan.tasks) >= SMALL_CALL_TASKS and not seen1   # auto: large call, none
+    assert len(res.plan.tasks) > LINK_BOUND_CALL_TASKS and not seen1   # auto: large call, none
