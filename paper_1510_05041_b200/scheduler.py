@@ -116,6 +116,10 @@ class RunOptions:
     trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
                                        # (resident arenas): X = alpha inv(E) B with inv(E)
                                        # computed once per diagonal tile; 0 = substitution
+    rampdown_tasks: int = 0            # wind-down batch: when at most this many tasks are
+                                       # left to start, start them all at once with
+                                       # ramp_chunk_steps-long launches (one GPU, resident
+                                       # arenas, no TRSM DAG); 0 = off
     prefetch: int = -1                 # 1: load every input tile at the call's start in
                                        # first-use order (one GPU, resident issue engine);
                                        # -1 = auto (scheduler.small_call), 0 off
@@ -323,6 +327,8 @@ class _GpuWorker:
         self._task_misses = 0
         self.chunk_steps = opts.chunk_steps
         self._ramp_left = max(0, opts.ramp_tasks)
+        # wind-down batch: one GPU, resident arenas, no DAG (set by run_plan)
+        self._rampdown = 0
         grp = runtime.topology.peer_group_of(desc)
         self._group_peers = frozenset(d.device_id for d in runtime.topology.devices
                                       if d.device_id != desc.device_id
@@ -483,6 +489,16 @@ class _GpuWorker:
 
     def fill(self) -> bool:
         fresh = []
+        if self._rampdown > 0:
+            # wind-down batch (RunOptions.rampdown_tasks): once at most that many tasks are
+            # left to start, start them all at once in extra slots with short launches
+            # issued k-major, so the call ends on many tasks' last steps instead of a few
+            # tasks' whole k-loops
+            left = len(self.runtime.queue) + self.rs.pending_count()
+            if 0 < left <= self._rampdown:
+                self.active.extend([None] * left)
+                self._ramp_left = left
+                self._rampdown = 0
         # ramp tasks (start-up batch) use extra slots; the others are capped at base_slots
         normal = sum(1 for a in self.active if a is not None and not a.ramp)
         for s, act in enumerate(self.active):
@@ -1341,7 +1357,8 @@ def _auto_arena_bytes(plan: TaskPlan, options: RunOptions, free_bytes: Optional[
         per_col_tile = rows_full * device_ld(t) + (device_ld(rem) if rem else 0)
         want += -(-per_col_tile * t * col_tiles * esz // 256) * 256 + 256 * col_tiles * (rows_full + 1)
     per_tile = device_ld(t) * t * esz
-    slots = options.n_streams * options.tasks_per_stream + max(0, options.ramp_tasks)
+    slots = (options.n_streams * options.tasks_per_stream + max(0, options.ramp_tasks)
+             + max(0, options.rampdown_tasks))
     want += (slots + 2) * 2 * per_tile + (64 << 20)
     if plan.call.kind == "trsm" and options.trsm_inverse_min:
         want += -(-plan.call.a.matrix.rows // t) * per_tile      # one inverse per diagonal tile
@@ -1482,6 +1499,9 @@ def _run_plan(plan: TaskPlan, topology: Optional[Topology], options: Optional[Ru
         # until the write-back lands): one GPU, or L2 on with every GPU in one peer group
         w._early_release = (w.resident and w._retain and options.release_on_issue
                             and (len(devs) == 1 or (options.l2_enabled and w._one_group)))
+        if (w.resident and len(devs) == 1 and options.rampdown_tasks > 0
+                and plan.call.kind != "trsm"):
+            w._rampdown = options.rampdown_tasks
         if not w.resident:
             w._ramp_left = 0      # the start-up batch is for resident arenas only
             # an evicting arena must hold every in-flight task's C and one launch's inputs

@@ -555,3 +555,23 @@ def test_prefetch_only_on_one_gpu_and_small_calls():
     eng1.ic_resolve = lambda *a: (seen1.append(a), orig1(*a))[1]
     res = run_call(big, Topology([DeviceDesc(0)]), RunOptions(), engine=eng1)
     assert len(res.plan.tasks) > LINK_BOUND_CALL_TASKS and not seen1   # auto: large call, none
+
+
+@pytest.mark.parametrize("kind", ["gemm", "syrk", "syr2k", "symm", "trmm"])
+def test_rampdown_batch_matches_reference(kind):
+    """RunOptions.rampdown_tasks: the last tasks start together in extra slots with short
+    launches; same results, every task once."""
+    call = build_call(kind, m=192, n=192, k=96, tile_size=24, seed=8, beta=1.0 if kind != "trmm" else 0.0,
+                      uplo="lower", trsm_scaled=True)
+    a = call.a.matrix.as_2d().copy()
+    b = call.b.matrix.as_2d().copy() if call.b is not None else None
+    c0 = call.c.matrix.as_2d().copy()
+    eng = FakeEngine(1, seed=21, arena_bytes=1 << 26)
+    res = run_call(call, Topology([DeviceDesc(0)]),
+                   RunOptions(rampdown_tasks=12, ramp_chunk_steps=1, prefetch=0), engine=eng)
+    assert sum(res.tasks_by_device.values()) == len(res.plan.tasks)
+    from oracle import tiled as OT
+    ref = c0.copy()
+    OT.run_tiled(kind, a, ref, b, tile_size=24, alpha=1.0, beta=1.0 if kind != "trmm" else 0.0,
+                 uplo="lower")
+    np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-11, atol=1e-11)
