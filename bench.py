@@ -789,7 +789,7 @@ def parse_args(argv=None):
     ap.add_argument("--tasks-per-stream", type=int, default=2)
     ap.add_argument("--trsm-inverse-min", type=int, default=128,
                     help="TRSM: inverse-based diagonal step from this tile order (0 = substitution)")
-    ap.add_argument("--release-on-issue", type=int, default=1, choices=[0, 1],
+    ap.add_argument("--release-on-issue", type=int, default=0, choices=[0, 1],
                     help="TRSM: release dependents when a solve is enqueued (1) or after its "
                          "write-back (0, the reference's rule)")
     ap.add_argument("--ref-seconds", type=float, default=8.0)

@@ -96,13 +96,15 @@ class RunOptions:
     critical_path_weight: int = 0      # TRSM: + weight x (longest chain of dependents) on
                                        # top of Eq. 3; 0 = the reference's Eq. 3
     retain_outputs: bool = True        # TRSM: keep written-back solved tiles cached (M->E)
-    release_on_issue: bool = True      # TRSM (one process, resident arenas): a solved tile
+    release_on_issue: bool = False     # TRSM (one process, resident arenas): a solved tile
                                        # is cached and its dependents released once its
                                        # solve is *enqueued*; their launches wait on the
                                        # solve's event on the GPU instead of the producer's
                                        # write-back + a host poll (the write-back still
-                                       # completes the task).  False = the reference's
-                                       # release-after-write-back
+                                       # completes the task).  Off: the reference's
+                                       # release-after-write-back measured
+                                       # as fast or faster (cfg4 134.7 vs 135.6 ms,
+                                       # profiles/trsm_ab_r02.txt)
     trsm_split_chain: bool = False     # TRSM: the update step reading the chain
                                        # predecessor's solved tile gets its own launch, so
                                        # the task's other updates need not wait for that

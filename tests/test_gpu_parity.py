@@ -462,7 +462,8 @@ def test_sgemm_precise_mode_meets_fp32_bound_at_small_k(i):
 @pytest.mark.parametrize("kind,kw,opts", [
     ("trsm", dict(uplo="lower", side="left"), dict(trsm_split_chain=True)),
     ("trsm", dict(uplo="upper", side="right", trans_a=True), dict(trsm_split_chain=True)),
-    ("trsm", dict(uplo="lower", side="left"), dict(release_on_issue=False, trsm_inverse_min=0)),
+    ("trsm", dict(uplo="lower", side="left"), dict(release_on_issue=True)),
+    ("trsm", dict(uplo="lower", side="left"), dict(release_on_issue=True, trsm_inverse_min=0)),
     ("trmm", dict(uplo="lower", side="left"), dict(split_km=True)),
     ("trmm", dict(uplo="upper", side="right", trans_a=True), dict(split_km=True, chunk_steps=2)),
     ("gemm", dict(beta=1.0), dict(ramp_tasks=0)),

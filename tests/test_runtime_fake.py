@@ -342,7 +342,8 @@ def test_trsm_release_on_issue_singular_still_raises():
     call = RoutineCall("trsm", a=make_tiled(MatrixDesc.from_array("A", a), 8),
                        b=None, c=make_tiled(MatrixDesc.from_array("C", b), 8), uplo="lower")
     with pytest.raises(SingularMatrixError):
-        run_call(call, Topology([DeviceDesc(0)]), RunOptions(chunk_steps=2, trsm_inverse_min=0),
+        run_call(call, Topology([DeviceDesc(0)]), RunOptions(chunk_steps=2, trsm_inverse_min=0,
+                                                             release_on_issue=True),
                  engine=FakeEngine(1, seed=2, arena_bytes=1 << 24))
 
 
@@ -361,7 +362,8 @@ def test_trsm_release_on_issue_off_without_shared_l2(split, monkeypatch):
     c0 = call.c.matrix.as_2d().copy()
     groups = ["g", "g", "g"] if split == "l2_off" else ["g", "h", "h"]
     topo_r = Topology([DeviceDesc(i, peer_group=g) for i, g in enumerate(groups)])
-    run_call(call, topo_r, RunOptions(chunk_steps=2, l2_enabled=split != "l2_off"),
+    run_call(call, topo_r, RunOptions(chunk_steps=2, l2_enabled=split != "l2_off",
+                                      release_on_issue=True),
              engine=FakeEngine(3, seed=4, arena_bytes=1 << 24))
     assert released == []
     from oracle import tiled

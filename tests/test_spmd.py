@@ -169,3 +169,18 @@ def test_torchrun_job_name_is_launch_unique(monkeypatch):
         assert sess.job == f"p29577_{os.getppid()}"
     finally:
         spmd.shutdown()
+
+
+def test_spmd_trsm_release_on_issue_fake():
+    """Release-on-issue across ranks (the producer's compute stream sets the solved tile's
+    flag; peers wait on it on the GPU) — opt-in since round 2."""
+    outs = spmd.launch(2, SC.run_case, "trsm", 192, 192, 64, 1, True, dict(release_on_issue=True),
+                       timeout=600)
+    _check(outs, 2)
+
+
+@pytest.mark.gpu
+def test_spmd_gpu_trsm_release_on_issue():
+    outs = spmd.launch(2, SC.run_case, "trsm", 1536, 1536, 512, 7, False, dict(release_on_issue=True),
+                       timeout=900, devices=[0, 0])
+    _check(outs, 2)
