@@ -1,7 +1,7 @@
 """Interleaved A/B of RunOptions sets on one host-resident call (device-event time per call,
 sets alternated round by round so clock / thermal drift hits every set alike).
 python tools/opts_ab.py kind n k tile rounds 'dict(...)' 'dict(...)' ...
-(BX_IC=0 etc. apply to every set; prints min / median ms and TF/s per set)"""
+(BX_IC=0 etc. apply to every set; BX_F32=1: SGEMM; prints min / median ms and TF/s per set)"""
 import statistics
 import sys
 
@@ -11,9 +11,11 @@ from paper_1510_05041_b200.engine import get_engine  # noqa: E402
 
 kind, n, k, t, rounds = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
 sets = [eval(x) for x in sys.argv[6:]] or [{}]
+import os  # noqa: E402
+import numpy as np  # noqa: E402
 call = build_call(kind, m=n, n=n, k=k, tile_size=t, seed=0, alpha=1.0,
                   beta=1.0 if kind in ("gemm", "syrk", "syr2k", "symm") else 0.0, uplo="lower",
-                  trsm_scaled=True)
+                  trsm_scaled=True, **({"dtype": np.float32} if os.environ.get("BX_F32") else {}))
 eng = get_engine([0])
 for x in [y for y in (call.a, call.b, call.c) if y is not None]:
     eng.register_host(x.matrix.storage)
