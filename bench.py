@@ -749,7 +749,8 @@ def spmd_bench(args, cfg):
     if r == 0:
         parity = parity_check(call, c0)
         line = result_line(args, cfg, val, e2e, kern, peak_v, clk, None, links, parity,
-                           execution=f"one process per GPU ({W} ranks, spmd runtime)")
+                           execution=f"one process per GPU ({W} ranks, spmd runtime, input tiles "
+                                     f"dealt to the ranks' host links: owner prefetch)")
         if not args.no_cpu_baseline and W == 1:
             line["cpu_baseline"] = {k: v for k, v in cpu_sample(cfg, call, args.cpu_seconds).items()
                                     if k in ("value", "unit", "cores", "kind", "sample")}

@@ -125,6 +125,10 @@ class RunOptions:
     prefetch: int = -1                 # 1: load every input tile at the call's start in
                                        # first-use order (one GPU, resident issue engine);
                                        # -1 = auto (scheduler.small_call), 0 off
+    owner_prefetch: bool = True        # one process per GPU (W >= 2, L2 on): deal the
+                                       # input tiles round-robin in first-use order to the
+                                       # ranks, each loads its share over its own host link
+                                       # at the call's start (spmd.py owner_prefetch)
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 

@@ -657,6 +657,64 @@ def _build_runtime_classes():
             self._permanent.append(blk)
             return blk
 
+        def owner_prefetch(self) -> int:
+            """Balanced host traffic (RunOptions.owner_prefetch): the call's input tiles, in
+            the order the tasks first read them (Morton task order, then step order), are
+            dealt round-robin to the ranks; at the call's start every rank claims its share
+            in the first-holder directory and enqueues their host loads on its own link,
+            with an arrival flag per tile.  Every rank's tasks then copy those tiles from
+            their owners over NVLink (waiting on the flags on the GPU) — each tile still
+            crosses a host link once, and the W links carry 1/W of the bytes each, whatever
+            order the dynamic schedule takes.  Without it the first rank to need a tile
+            fetches it, which can load one link with several times the mean (the fake-engine
+            run in tools/spmd_balance.py: max/mean 2.7 at 8 ranks).  Returns the tiles
+            fetched."""
+            W, r = self.W, self.rank
+            if W < 2 or not self.runtime.options.l2_enabled:
+                return 0
+            cb = self.blk
+            out_id = self.plan.call.c.matrix.matrix_id
+            seen = set()
+            n = fetched = 0
+            for task in self.plan.tasks:
+                for key, (ref, _m) in S.task_keys(task).items():
+                    if key in seen or key[0] == out_id or key[0] not in self.tbase:
+                        continue
+                    seen.add(key)
+                    mine = n % W == r
+                    n += 1
+                    if not mine or self.cache.contains(key):
+                        continue
+                    idx = self._kidx(key)
+                    if atomic_cas(cb.owner, idx, 0, r + 1) != 0:
+                        continue                 # another rank's task got there first
+                    h, w = ref.phys_height, ref.phys_width
+                    ld = S.device_ld(h)
+                    nbytes = ld * w * self.esz
+                    try:
+                        off = self.arena.alloc(nbytes)
+                    except S.ArenaOutOfMemoryError:
+                        raise CapacityDeadlockError(
+                            f"rank {r}: resident arena exhausted; spmd execution needs the "
+                            f"working set to fit in HBM") from None
+                    blk = LruBlock(key, off, nbytes, ld, self.device_id)
+                    blk.reader = 1
+                    payload = h * w * self.esz
+                    cb.offs[idx * W + r] = off + 1
+                    desc, r0, c0 = self._host_of(ref)
+                    blk.ready_ev = self._timed(S.LANE_H2D, lambda wt: self.eng.h2d(
+                        self.slot, off, ld, desc, r0, c0, h, w, wt), (), "H2D", payload)
+                    self.eng.write_flag(self.slot, S.LANE_H2D, self.flags_dptr + 4 * (idx * W + r), 1)
+                    self.dm.h2d_bytes += payload
+                    self.host_fetches += 1
+                    self._pending_keys.add(key)
+                    with self.cache.lock:
+                        self.cache._blocks[key] = blk
+                    self.runtime.directory.add_holder(key, self.device_id)
+                    self._permanent.append(blk)
+                    fetched += 1
+            return fetched
+
         def _retain_on_issue(self, act) -> None:
             """Release-on-issue (one process per GPU): cache the solved tile locally (base
             class), publish its arena offset, and have this task's compute stream set the
@@ -796,6 +854,8 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
     t_setup = t0 - t_setup0
     err = None
     try:
+        if options.owner_prefetch:
+            w.owner_prefetch()
         _drive(rt, w, sess)
     except BaseException as exc:   # abort every rank; reported after the end barrier
         err = exc

@@ -184,3 +184,35 @@ def test_spmd_gpu_trsm_release_on_issue():
     outs = spmd.launch(2, SC.run_case, "trsm", 1536, 1536, 512, 7, False, dict(release_on_issue=True),
                        timeout=900, devices=[0, 0])
     _check(outs, 2)
+
+
+@pytest.mark.parametrize("kind,n,k,tile,extra", CASES)
+def test_spmd_owner_prefetch_fake_three_ranks(kind, n, k, tile, extra):
+    """RunOptions.owner_prefetch: input tiles dealt round-robin to the ranks and loaded at
+    the call's start; every routine family still matches the oracle, every input tile
+    crosses a host link once, every task runs once."""
+    outs = spmd.launch(3, SC.run_case, kind, n, k, tile, 2, True, dict(owner_prefetch=True), extra,
+                       timeout=600)
+    _check(outs, 3)
+
+
+def test_spmd_owner_prefetch_balances_host_links():
+    """With owner prefetch the input (A/B) host bytes split evenly over the ranks' links."""
+    import balance_case as BC
+    outs = spmd.launch(4, BC.input_bytes_by_rank, 256, 32, timeout=600)
+    per = outs[0]
+    assert sum(per.values()) == 2 * 256 * 256 * 8          # A and B, each tile once
+    assert max(per.values()) <= 1.25 * (sum(per.values()) / len(per)), per
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,k,tile,extra", [
+    ("gemm", 1536, 1280, 512, {}),
+    ("syr2k", 1280, 768, 512, {}),
+    ("trmm", 1536, 1536, 512, {}),
+    ("trsm", 1536, 1536, 512, {}),
+])
+def test_spmd_gpu_owner_prefetch(kind, n, k, tile, extra):
+    outs = spmd.launch(2, SC.run_case, kind, n, k, tile, 5, False, dict(owner_prefetch=True), extra,
+                       timeout=900, devices=[0, 0])
+    _check(outs, 2)
