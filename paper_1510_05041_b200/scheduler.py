@@ -127,8 +127,10 @@ class RunOptions:
                                        # -1 = auto (scheduler.small_call), 0 off
     owner_prefetch: bool = True        # one process per GPU (W >= 2, L2 on): deal the
                                        # input tiles round-robin in first-use order to the
-                                       # ranks, each loads its share over its own host link
-                                       # at the call's start (spmd.py owner_prefetch)
+                                       # ranks, each loads its share over its own host link,
+                                       # at most owner_prefetch_mb ahead (spmd.py)
+    owner_prefetch_mb: int = 256       # the per-rank window of owner loads in flight, so a
+                                       # task's own C tile never queues behind all of them
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
 

@@ -657,63 +657,81 @@ def _build_runtime_classes():
             self._permanent.append(blk)
             return blk
 
-        def owner_prefetch(self) -> int:
+        def owner_plan(self) -> None:
             """Balanced host traffic (RunOptions.owner_prefetch): the call's input tiles, in
             the order the tasks first read them (Morton task order, then step order), are
-            dealt round-robin to the ranks; at the call's start every rank claims its share
-            in the first-holder directory and enqueues their host loads on its own link,
-            with an arrival flag per tile.  Every rank's tasks then copy those tiles from
-            their owners over NVLink (waiting on the flags on the GPU) — each tile still
-            crosses a host link once, and the W links carry 1/W of the bytes each, whatever
-            order the dynamic schedule takes.  Without it the first rank to need a tile
-            fetches it, which can load one link with several times the mean (the fake-engine
-            run in tools/spmd_balance.py: max/mean 2.7 at 8 ranks).  Returns the tiles
-            fetched."""
+            dealt round-robin to the ranks.  Each rank loads its share over its own host link
+            (``owner_step``), claiming each tile in the first-holder directory and raising
+            its arrival flag after the copy; the other ranks' tasks copy it from the owner
+            over NVLink, waiting on the flag on the GPU.  Every tile still crosses a host link
+            once, and the W links carry 1/W of the input bytes each whatever order the dynamic
+            schedule takes — without it the first rank to need a tile fetches it, which can
+            load one link with several times the mean (tools/spmd_balance.py: max/mean 2.4
+            at 8 ranks on the fake engine).  A tile some task needs before its owner got to
+            it is fetched by that task's rank as before (the owner then skips it)."""
             W, r = self.W, self.rank
+            self._owned, self._owned_next, self._owned_inflight = [], 0, []
             if W < 2 or not self.runtime.options.l2_enabled:
-                return 0
-            cb = self.blk
+                return
             out_id = self.plan.call.c.matrix.matrix_id
             seen = set()
-            n = fetched = 0
+            n = 0
             for task in self.plan.tasks:
                 for key, (ref, _m) in S.task_keys(task).items():
                     if key in seen or key[0] == out_id or key[0] not in self.tbase:
                         continue
                     seen.add(key)
-                    mine = n % W == r
+                    if n % W == r:
+                        self._owned.append((key, ref))
                     n += 1
-                    if not mine or self.cache.contains(key):
-                        continue
-                    idx = self._kidx(key)
-                    if atomic_cas(cb.owner, idx, 0, r + 1) != 0:
-                        continue                 # another rank's task got there first
-                    h, w = ref.phys_height, ref.phys_width
-                    ld = S.device_ld(h)
-                    nbytes = ld * w * self.esz
-                    try:
-                        off = self.arena.alloc(nbytes)
-                    except S.ArenaOutOfMemoryError:
-                        raise CapacityDeadlockError(
-                            f"rank {r}: resident arena exhausted; spmd execution needs the "
-                            f"working set to fit in HBM") from None
-                    blk = LruBlock(key, off, nbytes, ld, self.device_id)
-                    blk.reader = 1
-                    payload = h * w * self.esz
-                    cb.offs[idx * W + r] = off + 1
-                    desc, r0, c0 = self._host_of(ref)
-                    blk.ready_ev = self._timed(S.LANE_H2D, lambda wt: self.eng.h2d(
-                        self.slot, off, ld, desc, r0, c0, h, w, wt), (), "H2D", payload)
-                    self.eng.write_flag(self.slot, S.LANE_H2D, self.flags_dptr + 4 * (idx * W + r), 1)
-                    self.dm.h2d_bytes += payload
-                    self.host_fetches += 1
-                    self._pending_keys.add(key)
-                    with self.cache.lock:
-                        self.cache._blocks[key] = blk
-                    self.runtime.directory.add_holder(key, self.device_id)
-                    self._permanent.append(blk)
-                    fetched += 1
-            return fetched
+            tile_bytes = S.device_ld(self.plan.tile_size) * self.plan.tile_size * self.esz
+            self._owned_window = max(4, (self.runtime.options.owner_prefetch_mb << 20) // tile_bytes)
+
+        def owner_step(self) -> bool:
+            """Issue owner loads while fewer than the window are in flight on this rank's
+            host link (so a task's own C tile never queues behind the whole share)."""
+            if not self._owned or self._owned_next >= len(self._owned):
+                return False
+            live = [e for e in self._owned_inflight if not self.eng.done(e)]
+            self._owned_inflight = live
+            issued = False
+            W, r = self.W, self.rank
+            cb = self.blk
+            while len(self._owned_inflight) < self._owned_window and self._owned_next < len(self._owned):
+                key, ref = self._owned[self._owned_next]
+                self._owned_next += 1
+                if self.cache.contains(key):
+                    continue
+                idx = self._kidx(key)
+                if atomic_cas(cb.owner, idx, 0, r + 1) != 0:
+                    continue                     # a task got there first
+                h, w = ref.phys_height, ref.phys_width
+                ld = S.device_ld(h)
+                nbytes = ld * w * self.esz
+                try:
+                    off = self.arena.alloc(nbytes)
+                except S.ArenaOutOfMemoryError:
+                    raise CapacityDeadlockError(
+                        f"rank {r}: resident arena exhausted; spmd execution needs the "
+                        f"working set to fit in HBM") from None
+                blk = LruBlock(key, off, nbytes, ld, self.device_id)
+                blk.reader = 1
+                payload = h * w * self.esz
+                cb.offs[idx * W + r] = off + 1
+                desc, r0, c0 = self._host_of(ref)
+                blk.ready_ev = self._timed(S.LANE_H2D, lambda wt: self.eng.h2d(
+                    self.slot, off, ld, desc, r0, c0, h, w, wt), (), "H2D", payload)
+                self.eng.write_flag(self.slot, S.LANE_H2D, self.flags_dptr + 4 * (idx * W + r), 1)
+                self.dm.h2d_bytes += payload
+                self.host_fetches += 1
+                self._pending_keys.add(key)
+                with self.cache.lock:
+                    self.cache._blocks[key] = blk
+                self.runtime.directory.add_holder(key, self.device_id)
+                self._permanent.append(blk)
+                self._owned_inflight.append(blk.ready_ev)
+                issued = True
+            return issued
 
         def _retain_on_issue(self, act) -> None:
             """Release-on-issue (one process per GPU): cache the solved tile locally (base
@@ -855,7 +873,7 @@ def run_plan_spmd(plan, options, engine=None, session: Optional[Session] = None,
     err = None
     try:
         if options.owner_prefetch:
-            w.owner_prefetch()
+            w.owner_plan()
         _drive(rt, w, sess)
     except BaseException as exc:   # abort every rank; reported after the end barrier
         err = exc
@@ -947,15 +965,22 @@ def _gather_metrics(plan, blk, W, wall) -> Metrics:
 
 def _drive(rt, w, sess) -> None:
     eng = rt.engine
+    owned = getattr(w, "_owned", None)
+    if owned:
+        w.owner_step()                    # the first window goes out before any task
     while not rt.done():
         if sess.aborted():
             raise _PeerFailed("spmd: another rank failed")
         progressed = w.poll()
         progressed |= w.fill()
+        if owned:
+            progressed |= w.owner_step()
         if rt.done():
             break
         if not progressed:
             evs = w.in_flight()
+            if owned and w._owned_inflight and w._owned_next < len(owned):
+                evs = list(evs) + w._owned_inflight[:1]
             if evs:
                 eng.wait_any(evs, spin_us=200)
             else:

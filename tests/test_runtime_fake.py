@@ -547,9 +547,10 @@ def test_prefetch_only_on_one_gpu_and_small_calls():
     seen = []
     orig = eng.ic_resolve
     eng.ic_resolve = lambda *a: (seen.append(a), orig(*a))[1]
-    run_call(call, Topology([DeviceDesc(i, peer_group="g") for i in range(2)]), RunOptions(prefetch=1),
-             engine=eng)
+    run_call(call, Topology([DeviceDesc(i, peer_group="g") for i in range(2)]),
+             RunOptions(prefetch=1), engine=eng)
     assert not seen                                # two GPUs: no prefetch
+
     big = build_call("gemm", m=12 * 24, n=12 * 24, k=48, tile_size=24, seed=2, beta=0.0)
     eng1 = FakeEngine(1, seed=1, arena_bytes=1 << 24)
     seen1 = []
