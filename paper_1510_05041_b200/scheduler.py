@@ -118,6 +118,8 @@ class RunOptions:
     trsm_inverse_min: int = 128        # TRSM diagonal steps on tiles of at least this order
                                        # (resident arenas): X = alpha inv(E) B with inv(E)
                                        # computed once per diagonal tile; 0 = substitution
+    prefetch_window_mb: int = 0        # large one-GPU calls: keep this much of first-use
+                                       # tile loads in flight ahead of the tasks (0 = off)
     rampdown_tasks: int = 0            # wind-down batch: when at most this many tasks are
                                        # left to start, start them all at once with
                                        # ramp_chunk_steps-long launches (one GPU, resident
@@ -335,6 +337,8 @@ class _GpuWorker:
         self._task_misses = 0
         self.chunk_steps = opts.chunk_steps
         self._ramp_left = max(0, opts.ramp_tasks)
+        self._pf = None               # windowed first-use prefetch (large one-GPU calls)
+        self._pf_next, self._pf_events = 0, []
         # wind-down batch: one GPU, resident arenas, no DAG (set by run_plan)
         self._rampdown = 0
         grp = runtime.topology.peer_group_of(desc)
@@ -494,6 +498,25 @@ class _GpuWorker:
                 e.priority = self._priority(e.task)
                 e.pver = ver
         return self.rs.pop_best()
+
+    def prefetch_step(self) -> bool:
+        """Windowed first-use prefetch (RunOptions.prefetch_window_mb, one GPU, large
+        calls): keep loading input tiles in the order the tasks first read them, in
+        batches of 8 with one arrival event each, while less than the window is in flight
+        on the H2D lane.  Tiles a task already fetched are L1 hits and skipped by C."""
+        pf = self._pf
+        if pf is None or self._pf_next >= len(pf[0]):
+            return False
+        order, window = pf
+        self._pf_events = [e for e in self._pf_events if not self.eng.done(e)]
+        issued = False
+        while len(self._pf_events) * 8 < window and self._pf_next < len(order):
+            batch = order[self._pf_next:self._pf_next + 8]
+            self._pf_next += len(batch)
+            _offs, _lds, waits = self.eng.ic_resolve(self.ic, self.ic_d, array("i", batch))
+            self._pf_events.extend(waits[-1:])
+            issued = True
+        return issued
 
     def fill(self) -> bool:
         fresh = []
@@ -1319,6 +1342,22 @@ def _ic_prefetch(plan, options, workers, engine) -> None:
     want = options.prefetch
     if want < 0:
         want = small_call(plan)
+    if len(workers) == 1 and workers[0].ic is not None and not want and options.prefetch_window_mb > 0:
+        # large call: a window of first-use loads kept ahead of the tasks (prefetch_step)
+        w = workers[0]
+        seen, order = set(), []
+        for task in plan.tasks:
+            tids, _mult = ic_task_tiles(task)
+            for t in tids:
+                t = int(t)
+                if t not in seen:
+                    seen.add(t)
+                    order.append(t)
+        tile_bytes = device_ld(plan.tile_size) * plan.tile_size * plan.dtype.itemsize
+        w._pf = (order, max(8, (options.prefetch_window_mb << 20) // tile_bytes))
+        w._pf_next, w._pf_events = 0, []
+        w.prefetch_step()
+        return
     if not want or len(workers) != 1 or workers[0].ic is None:
         return
     w = workers[0]
@@ -1620,10 +1659,13 @@ def _drive_single(rt: _Runtime, workers) -> None:
             progressed |= w.poll()
         for w in workers:
             progressed |= w.fill()
+            if w._pf is not None:
+                progressed |= w.prefetch_step()
         if rt.done():
             break
         if not progressed:
             evs = [e for w in workers for e in w.in_flight()]
+            evs += [w._pf_events[0] for w in workers if w._pf_events and w._pf_next < len(w._pf[0])]
             if not evs:
                 raise RuntimeError("runtime stalled: tasks remain but nothing is in flight")
             eng.wait_any(evs, spin_us=2000)

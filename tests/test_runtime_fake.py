@@ -578,3 +578,20 @@ def test_rampdown_batch_matches_reference(kind):
     OT.run_tiled(kind, a, ref, b, tile_size=24, alpha=1.0, beta=1.0 if kind != "trmm" else 0.0,
                  uplo="lower")
     np.testing.assert_allclose(call.c.matrix.as_2d(), ref, rtol=1e-11, atol=1e-11)
+
+
+@pytest.mark.parametrize("kind", ["gemm", "syrk", "syr2k", "symm"])
+def test_prefetch_window_large_call(kind):
+    """RunOptions.prefetch_window_mb on a large one-GPU call (> LINK_BOUND_CALL_TASKS tasks):
+    first-use loads kept ahead of the tasks; results and host bytes as without it."""
+    from paper_1510_05041_b200.scheduler import LINK_BOUND_CALL_TASKS
+    call = build_call(kind, m=12 * 16, n=12 * 16, k=64, tile_size=16, seed=3, beta=1.0, uplo="lower")
+    c0 = call.c.matrix.as_2d().copy()
+    topo1 = Topology([DeviceDesc(0)])
+    res = run_call(call, topo1, RunOptions(prefetch_window_mb=1), engine=FakeEngine(1, seed=5, arena_bytes=1 << 24))
+    out = call.c.matrix.as_2d().copy()
+    call.c.matrix.as_2d()[:] = c0
+    ref = run_call(call, topo1, RunOptions(), engine=FakeEngine(1, seed=6, arena_bytes=1 << 24))
+    assert len(res.plan.tasks) > LINK_BOUND_CALL_TASKS or kind in ("syrk", "syr2k")
+    np.testing.assert_allclose(out, call.c.matrix.as_2d(), rtol=1e-12, atol=1e-12)
+    assert res.metrics.total_h2d_bytes() == ref.metrics.total_h2d_bytes()
