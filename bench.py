@@ -573,7 +573,9 @@ def single_bench(args, cfg):
     topo = Topology([DeviceDesc(g, peer_group="nvlink") for g in range(args.gpus)])
     opts = RunOptions(chunk_steps=args.chunk, n_streams=args.streams,
                       tasks_per_stream=args.tasks_per_stream, trsm_inverse_min=args.trsm_inverse_min,
-                      release_on_issue=bool(args.release_on_issue))
+                      release_on_issue=bool(args.release_on_issue),
+                      owner_prefetch=args.owner_prefetch_mb > 0,
+                      owner_prefetch_mb=max(1, args.owner_prefetch_mb))
     for mt in (call.a, call.b, call.c):
         if mt is not None:
             eng.register_host(mt.matrix.storage)   # page-locking excluded
@@ -683,7 +685,9 @@ def spmd_bench(args, cfg):
             eng.register_host(mt.matrix.storage)   # page-locking excluded from timing
     opts = RunOptions(execution="spmd", chunk_steps=args.chunk, n_streams=args.streams,
                       tasks_per_stream=args.tasks_per_stream, trsm_inverse_min=args.trsm_inverse_min,
-                      release_on_issue=bool(args.release_on_issue))
+                      release_on_issue=bool(args.release_on_issue),
+                      owner_prefetch=args.owner_prefetch_mb > 0,
+                      owner_prefetch_mb=max(1, args.owner_prefetch_mb))
     for _ in range(args.warmup):
         run_call(call, options=opts)
     # links with all ranks active: H2D/D2H of this rank's lanes, P2P from the next rank's
@@ -793,6 +797,9 @@ def parse_args(argv=None):
     ap.add_argument("--release-on-issue", type=int, default=0, choices=[0, 1],
                     help="TRSM: release dependents when a solve is enqueued (1) or after its "
                          "write-back (0, the reference's rule)")
+    ap.add_argument("--owner-prefetch-mb", type=int, default=64,
+                    help="one process per GPU: owner loads in flight per rank (0 = plain "
+                         "first-holder fetches)")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

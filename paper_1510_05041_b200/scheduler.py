@@ -131,7 +131,7 @@ class RunOptions:
                                        # input tiles round-robin in first-use order to the
                                        # ranks, each loads its share over its own host link,
                                        # at most owner_prefetch_mb ahead (spmd.py)
-    owner_prefetch_mb: int = 256       # the per-rank window of owner loads in flight, so a
+    owner_prefetch_mb: int = 64        # the per-rank window of owner loads in flight, so a
                                        # task's own C tile never queues behind all of them
     arena_bytes: int = 0               # per GPU; 0 = sized for the call
 
