@@ -10,11 +10,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def rank_main(calls):
+def rank_main(calls, n=512, t=256):
     import numpy as np
     from paper_1510_05041_b200 import RunOptions, build_call, run_call, spmd
     sess = spmd.current()
-    call = build_call("gemm", m=512, n=512, k=512, tile_size=256, seed=0, beta=1.0) if sess.rank == 0 else None
+    call = build_call("gemm", m=n, n=n, k=n, tile_size=t, seed=0, beta=1.0) if sess.rank == 0 else None
     call = sess.share_call(call)
     from paper_1510_05041_b200.engine import get_engine
     eng = get_engine([sess.rank], 4, [sess.device])
@@ -25,7 +25,7 @@ def rank_main(calls):
         run_call(call, options=opts)
     if os.environ.get("BX_PROF"):
         import cProfile
-        cProfile.runctx("for _ in range(20): run_call(call, options=opts)", globals(), locals(),
+        cProfile.runctx("for _ in range(int(os.environ.get('BX_PROF_CALLS', '20'))): run_call(call, options=opts)", globals(), locals(),
                         f"{os.environ['BX_PROF']}.{sess.rank}")
     ph, wall = {}, []
     for _ in range(calls):
@@ -42,8 +42,10 @@ def rank_main(calls):
 if __name__ == "__main__":
     ranks = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     calls = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 512
+    t = int(sys.argv[4]) if len(sys.argv) > 4 else 256
     from paper_1510_05041_b200 import RunOptions, build_call, run_call, spmd
-    call = build_call("gemm", m=512, n=512, k=512, tile_size=256, seed=0, beta=1.0)
+    call = build_call("gemm", m=n, n=n, k=n, tile_size=t, seed=0, beta=1.0)
     from paper_1510_05041_b200 import pin_host
     for t in (call.a, call.b, call.c):
         pin_host(t.matrix.storage)
@@ -60,5 +62,5 @@ if __name__ == "__main__":
                                **{k: round(statistics.median(v), 3) for k, v in ph.items()}}, flush=True)
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import spmd_overhead as me
-    for out in spmd.launch(ranks, me.rank_main, calls, devices=[0] * ranks):
+    for out in spmd.launch(ranks, me.rank_main, calls, n, t, devices=[0] * ranks):
         print(f"spmd {ranks} ranks:", out, flush=True)
